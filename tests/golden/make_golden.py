@@ -1,0 +1,225 @@
+"""Generate the golden vectors that pin the oracle (and, through it, the GPU
+path) to the reference implementation.
+
+Run HERE (the container that has /root/reference), never on the GPU box:
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONPATH=/root/reference/pkg/src \
+        python tests/golden/make_golden.py
+
+It imports the reference package ``cspq`` (read-only, untouched) and records
+its outputs on small seeded inputs into ``tests/golden/*.npz``.  The inputs
+mirror the reference's own hot-path tests (pkg/tests/test_kernels.py,
+test_bulk.py, test_training.py, test_acceptance.py) plus config-shaped cases
+(BASELINE.json configs 1-5 at reduced N).  Only the generated .npz files and
+this script are committed; nothing here is imported at test time.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ref():
+    sys.path.insert(0, "/root/reference/pkg/src")
+    import cspq  # noqa: F401
+    from cspq import bulk, core, kernels, training
+    return bulk, core, kernels, training
+
+
+def encode_cases(bulk, core, kernels):
+    EV = kernels.EncoderVariant
+    rng = np.random.default_rng(20260101)
+    out = {}
+
+    def put(name, X, rowmajor, in_u8=False):
+        cbs = [core.Codebook.from_rowmajor(j, rowmajor[j]) for j in range(rowmajor.shape[0])]
+        cset = bulk.CodebookSet.from_codebooks(cbs)
+        out[f"{name}/X"] = X
+        out[f"{name}/rowmajor"] = cset.rowmajor
+        out[f"{name}/biases"] = cset.biases
+        for var in (EV.REFERENCE, EV.REFORMULATED, EV.BLOCKED):
+            codes = bulk.encode_dataset(X, cset, bulk.ExecutionPlan(variant=var, w=16)).codes
+            out[f"{name}/codes_{var.value}"] = codes
+        out[f"{name}/codes_nobias"] = bulk.encode_dataset(
+            X, cset, bulk.ExecutionPlan(variant=EV.BLOCKED, w=8), precomputed_bias=False).codes
+        # winning scores (bitwise) for the first rows, via the per-subvector API
+        nb = min(64, X.shape[0])
+        sub = cset.sub_dim
+        best_reform = np.zeros((nb, cset.m), np.float32)
+        best_ref = np.zeros((nb, cset.m), np.float32)
+        for i in range(nb):
+            for j in range(cset.m):
+                v = np.asarray(X[i, j * sub:(j + 1) * sub], dtype=np.float32)
+                best_reform[i, j] = kernels.encode_reform_with_score(v, cset[j])[1]
+                best_ref[i, j] = kernels.encode_ref_with_score(v, cset[j])[1]
+        out[f"{name}/best_reformulated"] = best_reform
+        out[f"{name}/best_reference"] = best_ref
+
+    # random normal, generic shapes (test_kernels-style)
+    put("rand_m4_k256_s8", rng.standard_normal((3000, 32)).astype(np.float32),
+        rng.standard_normal((4, 256, 8)).astype(np.float32))
+    # remainder blocks / small k / odd sub (test_kernels.py:90-97)
+    put("rand_m3_k5_s4", rng.standard_normal((500, 12)).astype(np.float32),
+        rng.standard_normal((3, 5, 4)).astype(np.float32))
+    put("rand_m2_k7_s3", rng.standard_normal((500, 6)).astype(np.float32),
+        rng.standard_normal((2, 7, 3)).astype(np.float32))
+    put("rand_m1_k1_s6", rng.standard_normal((50, 6)).astype(np.float32),
+        rng.standard_normal((1, 1, 6)).astype(np.float32))
+    put("rand_m4_k33_s7", rng.standard_normal((500, 28)).astype(np.float32),
+        rng.standard_normal((4, 33, 7)).astype(np.float32))
+    put("rand_m2_k37_s16", rng.standard_normal((500, 32)).astype(np.float32),
+        rng.standard_normal((2, 37, 16)).astype(np.float32))
+    put("rand_m5_k64_s1", rng.standard_normal((400, 5)).astype(np.float32),
+        rng.standard_normal((5, 64, 1)).astype(np.float32))
+    put("rand_m3_k256_s2", rng.standard_normal((600, 6)).astype(np.float32),
+        rng.standard_normal((3, 256, 2)).astype(np.float32))
+    # uint16 codes (test_bulk.py:74-78)
+    put("rand_m2_k300_s4", rng.standard_normal((400, 8)).astype(np.float32),
+        rng.standard_normal((2, 300, 4)).astype(np.float32))
+    put("rand_m1_k1000_s8", rng.standard_normal((200, 8)).astype(np.float32),
+        rng.standard_normal((1, 1000, 8)).astype(np.float32))
+    # large dynamic range
+    put("scaled_m4_k256_s8", (rng.standard_normal((1000, 32)) * 1e3).astype(np.float32),
+        (rng.standard_normal((4, 256, 8)) * 1e3).astype(np.float32))
+    # config-1-like: integer data, codebook = distinct data subvectors (tie-heavy)
+    cent = rng.uniform(0, 255, size=(8, 128))
+    lab = rng.integers(0, 8, size=3000)
+    X1 = np.clip(np.rint(cent[lab] + rng.normal(0, 20, size=(3000, 128))), 0, 255).astype(np.float32)
+    rm = np.zeros((16, 256, 8), np.float32)
+    for j in range(16):
+        u = np.unique(X1[:, j * 8:(j + 1) * 8], axis=0)
+        rm[j] = u[rng.choice(u.shape[0], 256, replace=False)]
+    put("c1like_m16_k256_s8", X1, rm)
+    # config-4-like: uint8 input widened in the encoder, d_sub = 4
+    X4 = np.clip(np.rint(cent[lab][:, :128] + rng.normal(0, 15, size=(3000, 128))), 0, 255).astype(np.uint8)
+    rm4 = (rng.uniform(0, 255, size=(32, 256, 4))).astype(np.float32)
+    put("c4like_u8_m32_k256_s4", X4, rm4, in_u8=True)
+    # unit-normalised rows (configs 3/5)
+    X3 = rng.standard_normal((2000, 96)).astype(np.float32)
+    X3 /= np.linalg.norm(X3, axis=1, keepdims=True)
+    rm3 = rng.standard_normal((12, 256, 8)).astype(np.float32) * np.float32(0.2)
+    put("unit_m12_k256_s8", X3.astype(np.float32), rm3)
+    # duplicated centroids: exact ties -> smaller index (test_kernels.py:141-151)
+    rmt = rng.standard_normal((3, 32, 8)).astype(np.float32)
+    rmt[:, 20] = rmt[:, 3]
+    rmt[:, 31] = rmt[:, 0]
+    Xt = np.concatenate([rmt[0, [3, 0, 20, 31]].reshape(4, 8)] * 3, axis=1)
+    Xt = np.concatenate([Xt, rng.standard_normal((60, 24)).astype(np.float32)]).astype(np.float32)
+    put("ties_m3_k32_s8", Xt, rmt)
+    # non-finite rows: encode_dataset does not validate raw ndarrays
+    Xn = rng.standard_normal((40, 16)).astype(np.float32)
+    Xn[3, 2] = np.nan
+    Xn[5, :] = np.nan
+    Xn[7, 9] = np.inf
+    Xn[8, 1] = -np.inf
+    Xn[9, 0] = np.float32(3e38)
+    Xn[10, 12] = np.float32(1e-42)  # denormal
+    put("nonfinite_m2_k16_s8", Xn, rng.standard_normal((2, 16, 8)).astype(np.float32))
+    # known answers (test_kernels.py:37-88)
+    put("hand_blocked", np.array([[1, 0]], np.float32),
+        np.array([[[1, 0], [0, 1], [2, 0], [0, 0]]], np.float32))
+    put("hand_identity", np.array([[1, 0]], np.float32), np.array([[[3, 4]]], np.float32))
+    put("hand_pair", np.array([[0.6, 0.4]], np.float32), np.array([[[1, 0], [0, 1]]], np.float32))
+    return out
+
+
+def lloyd_cases(training):
+    TC = training.TrainConfig
+    rng = np.random.default_rng(777)
+    out = {}
+
+    def put(name, P64, init, iters, tol):
+        r = training.lloyd_iterate(P64, init, TC(k=init.shape[0], max_iters=iters, tol=tol))
+        out[f"{name}/pts"] = P64.astype(np.float32)
+        out[f"{name}/init"] = init
+        out[f"{name}/max_iters"] = np.int64(iters)
+        out[f"{name}/tol"] = np.float64(tol)
+        out[f"{name}/centroids"] = r.centroids
+        out[f"{name}/objectives"] = np.asarray(r.objectives, np.float64)
+        out[f"{name}/assignments"] = r.assignments
+        out[f"{name}/iterations"] = np.int64(r.iterations)
+
+    # empty-cluster repair (test_training.py:142-155)
+    P = np.array([[0.0], [0.1], [0.2], [10.0], [10.1], [50.0]], np.float32).astype(np.float64)
+    put("repair_1d", P, np.array([[0.0], [0.0], [10.0]]), 10, 1e-4)
+    # gaussian blobs, tol stop
+    means = rng.uniform(-5, 5, size=(16, 2))
+    P = (means[rng.integers(0, 16, 4000)] + rng.normal(0, 0.4, (4000, 2))).astype(np.float32).astype(np.float64)
+    put("blobs_k16_s2", P, P[rng.choice(4000, 16, replace=False)], 50, 1e-4)
+    # config-2-like (d_sub 8, k 256, sample-point init, tol 0)
+    cen = rng.uniform(0, 1, size=(64, 8))
+    P = np.clip(cen[rng.integers(0, 64, 12000)] + rng.normal(0, 0.08, (12000, 8)), 0, None)
+    P = P.astype(np.float32).astype(np.float64)
+    put("c2like_k256_s8", P, P[np.sort(rng.choice(12000, 256, replace=False))], 25, 0.0)
+    # config-3-like: unit-normalised embeddings
+    Z = rng.standard_normal((8000, 64))
+    Z /= np.linalg.norm(Z, axis=1, keepdims=True)
+    P = Z[:, 8:16].astype(np.float32).astype(np.float64)
+    put("c3like_k256_s8", P, P[np.sort(rng.choice(8000, 256, replace=False))], 10, 0.0)
+    # config-4-like: integer data, d_sub 4, duplicates -> empty-cluster repair
+    cen = rng.uniform(0, 255, size=(32, 4))
+    P = np.clip(np.rint(cen[rng.integers(0, 32, 10000)] + rng.normal(0, 15, (10000, 4))), 0, 255)
+    P = P.astype(np.float32).astype(np.float64)
+    init = P[np.sort(rng.choice(10000, 256, replace=False))].copy()
+    init[5] = init[4]  # guaranteed duplicate -> one empty cluster in iteration 1
+    put("c4like_k256_s4", P, init, 20, 0.0)
+    # k = 1 mean
+    P = np.array([[1.0, 5.0], [3.0, 5.0], [2.0, 8.0]], np.float64)
+    put("k1", P, P[:1].copy(), 5, 1e-4)
+    return out
+
+
+def train_cases(core, training):
+    """Reference default path (k-means++ seeding, per-subspace sampling)."""
+    rng = np.random.default_rng(4242)
+    out = {}
+    means = rng.uniform(-1, 1, size=(24, 32)).astype(np.float32)
+    X = (means[rng.integers(0, 24, 6000)] + rng.normal(0, 0.05, (6000, 32)).astype(np.float32)).astype(np.float32)
+    ds = core.VectorDataset(data=np.ascontiguousarray(X))
+    params = core.PQParams(d=32, m=4, k=64)
+    cfg = training.TrainConfig(k=64, seed=11, sample_cap=3000, max_iters=12)
+    cbs, reps = training.train_all_codebooks_report(ds, params, cfg)
+    out["kmpp/X"] = X
+    out["kmpp/centroids"] = np.stack([cb.centroids_rowmajor for cb in cbs])
+    out["kmpp/biases"] = np.stack([cb.biases for cb in cbs])
+    for j, r in enumerate(reps):
+        out[f"kmpp/objectives_{j}"] = np.asarray(r.objectives)
+        out[f"kmpp/assignments_{j}"] = r.assignments
+        out[f"kmpp/iterations_{j}"] = np.int64(r.iterations)
+    # the seeding alone, for one subspace (training.py:76-92)
+    rngs = training._subspace_rngs(11, 4)
+    pts = np.ascontiguousarray(X[:, 8:16])
+    sampled = training._sample(pts, 3000, rngs[1])
+    init = training._kmeanspp_init(sampled.astype(np.float64), 64, rngs[1])
+    out["kmpp/seed_init_sub1"] = init
+    return out
+
+
+def pairwise_cases():
+    rng = np.random.default_rng(5)
+    out = {}
+    for n in (0, 1, 7, 8, 9, 127, 128, 129, 1000, 8193, 100003):
+        a = rng.random(n) * rng.random(n) * 1e3
+        out[f"pw/{n}/a"] = a
+        out[f"pw/{n}/sum"] = np.float64(a.sum())
+    return out
+
+
+def main():
+    bulk, core, kernels, training = _ref()
+    np.savez_compressed(os.path.join(HERE, "encode_golden.npz"), **encode_cases(bulk, core, kernels))
+    np.savez_compressed(os.path.join(HERE, "lloyd_golden.npz"), **lloyd_cases(training))
+    np.savez_compressed(os.path.join(HERE, "train_golden.npz"), **train_cases(core, training))
+    np.savez_compressed(os.path.join(HERE, "pairwise_golden.npz"), **pairwise_cases())
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
+
+
+if __name__ == "__main__":
+    main()
