@@ -1,0 +1,213 @@
+/*
+ * cspq_b200.h -- C ABI of the B200-native PQ-construction engine.
+ *
+ * This is the drop-in boundary for the reference package `cspq`
+ * (/root/reference/pkg/src/cspq).  The reference has no FFI: its operator
+ * seam is the jitted bulk driver
+ *     _drive_chunk_major(X, b0, b1, CB, CT, B, w, variant, precomp, out)
+ *         kernels.py:271-316, called at bulk.py:145-148
+ * and the Lloyd assignment/update of training.py:57-159.  Each entry point
+ * below replaces one of those and cites it.  Python binds them with ctypes
+ * (paper_2605_25521_b200/_native.py); INTEGRATION.md shows the binding the
+ * reference side would add.
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes only; no torch types;
+ *   - device pointers unless the name says _host; caller-allocated;
+ *   - stream-ordered on `stream` (a cudaStream_t passed as void*, NULL =
+ *     legacy default stream); no hidden device synchronisation except where
+ *     documented (the _host pipeline is synchronous by contract);
+ *   - return 0 on success or a negative CSPQ_E* code; cspq_last_error()
+ *     returns a per-thread message for the last failure (like the
+ *     reference's ConfigError / DataError messages, core.py:14-44);
+ *   - re-entrant: concurrent calls on different streams are safe
+ *     (bulk.py:150-155 runs drivers concurrently on disjoint row ranges).
+ *
+ * Layouts (the reference's, bulk.py:53-81 and core.py:88-124):
+ *   X      (n, d) row-major, float32 or uint8 (uint8 is widened exactly to
+ *          float32 in-kernel; the reference widens on the host, bulk.py:125);
+ *          x_row_stride = elements between rows (>= d).
+ *   CB     (m, k, sub) float32 row-major centroids ("rowmajor").
+ *   B      (m, k) float32 biases 0.5*||c||^2 (compute_biases, core.py:232-243);
+ *          the bias bits are an input contract, never recomputed here.
+ *   codes  (n, m) row-major, uint8 when k <= 256 else uint16 (bulk.py:127).
+ */
+#ifndef CSPQ_B200_H
+#define CSPQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSPQ_ABI_VERSION 1
+
+/* error codes */
+#define CSPQ_OK 0
+#define CSPQ_E_CONFIG (-1)   /* bad shape / parameter   -> cspq ConfigError   */
+#define CSPQ_E_DATA (-2)     /* bad data                -> cspq DataError     */
+#define CSPQ_E_CUDA (-3)     /* CUDA runtime failure                          */
+#define CSPQ_E_NOMEM (-4)    /* allocation failure                            */
+#define CSPQ_E_TRAINING (-5) /* cannot train            -> cspq TrainingError */
+
+/* input element type of X */
+#define CSPQ_IN_F32 0
+#define CSPQ_IN_U8 1
+
+/* encoder variants (kernels.py:36-51 EncoderVariant / _VARIANT_IDS) */
+#define CSPQ_VARIANT_REFERENCE 0    /* (vv + cc) - 2 dd, kernels.py:84-105      */
+#define CSPQ_VARIANT_REFORMULATED 1 /* b - dd,            kernels.py:108-122     */
+#define CSPQ_VARIANT_BLOCKED 2      /* b - dd (== REFORMULATED bit for bit),
+                                       kernels.py:125-245                        */
+
+/* arithmetic modes; every mode returns the oracle's codes bit for bit */
+#define CSPQ_MODE_AUTO 0    /* fastest provably-exact path for the shape      */
+#define CSPQ_MODE_EXACT 1   /* strict fp32 mul-then-add chains, no FMA        */
+#define CSPQ_MODE_GUARDED 2 /* FFMA scores + error-bound guard + exact fix-up */
+
+int cspq_abi_version(void);
+const char *cspq_last_error(void);
+
+/* Guard constants of a codebook set: guard[2*j] = max_l |B[j,l]|,
+ * guard[2*j+1] = max_l ||CB[j,l,:]||_2 (rounded up).  Computed once per
+ * codebook set (the reference's "built once per train/load", bulk.py:55-58)
+ * and passed to cspq_encode; (m, 2) float32 device buffer. */
+int cspq_encode_prepare(const float *CB, const float *B, int32_t m, int32_t k, int32_t sub,
+                        float *guard, void *stream);
+
+/* Bias table of the precomputed_bias=False ablation (kernels.py:146-157):
+ * B_out[j,l] = 0.5f * fl-chain(sum_t c_t*c_t) in float32, exactly as the
+ * reference recomputes it per vector.  (m, k) float32 device buffer. */
+int cspq_recompute_biases_f32(const float *CB, int32_t m, int32_t k, int32_t sub, float *B_out,
+                              void *stream);
+
+/* Bulk encode of device-resident rows: replaces _drive_chunk_major over all
+ * blocks (kernels.py:271-316, bulk.py:139-155).  `guard` may be NULL (it is
+ * then computed on the stream with stream-ordered scratch).  B is ignored
+ * for CSPQ_VARIANT_REFERENCE.  codes_row_stride = elements between code rows
+ * (>= m). */
+int cspq_encode(const void *X, int32_t in_dtype, int64_t n, int32_t d, int64_t x_row_stride,
+                const float *CB, const float *B, const float *guard, int32_t m, int32_t k,
+                int32_t sub, void *codes, int64_t codes_row_stride, int32_t variant, int32_t mode,
+                void *stream);
+
+/* Exact encode that also returns each winning score -- the per-subvector
+ * API encode_*_with_score (kernels.py:349-404, the ScoreBlock best_score of
+ * core.py:183-201).  codes (n, m) int32, best (n, m) float32 (the oracle's
+ * score: b - dd for REFORMULATED/BLOCKED, (vv + cc) - 2 dd for REFERENCE). */
+int cspq_encode_with_scores(const void *X, int32_t in_dtype, int64_t n, int32_t d, int64_t x_row_stride,
+                            const float *CB, const float *B, int32_t m, int32_t k, int32_t sub,
+                            int32_t *codes, float *best, int32_t variant, void *stream);
+
+/* Same as cspq_encode for a subspace-major batch (m, n, sub) -- the layout
+ * of Lloyd's training sample -- writing codes as (m, n) int32.  This is the
+ * final REFERENCE-variant assignment pass of lloyd_iterate
+ * (training.py:143-150). */
+int cspq_encode_subspace_major(const float *P, int64_t n, int32_t m, int32_t sub, const float *CB,
+                               const float *B, int32_t k, int32_t *assign, int32_t variant,
+                               void *stream);
+
+/* End-to-end encode from HOST memory: pinned or pageable X (n, d) -> host
+ * codes (n, m), pipelined in batches of `batch_rows` over `n_streams` CUDA
+ * streams (H2D copy, encode, D2H copy overlapped; pageable buffers are
+ * staged through a pinned ring).  CB/B/guard are device pointers on
+ * `device`.  Synchronous: returns when codes are in host memory.
+ * batch_ms (optional, ceil(n / batch_rows) doubles) receives each batch's
+ * host-observed latency from its H2D enqueue to its codes landing in host
+ * memory (BASELINE config 5's per-batch p50/p99). */
+int cspq_encode_host(const void *X_host, int32_t in_dtype, int64_t n, int32_t d, const float *CB,
+                     const float *B, const float *guard, int32_t m, int32_t k, int32_t sub,
+                     void *codes_host, int32_t variant, int32_t mode, int64_t batch_rows,
+                     int32_t n_streams, double *batch_ms, int32_t device);
+
+/* ---------------- Lloyd k-means (training.py:57-159), all M subspaces at once.
+ * P      (m, n, sub) training points, float32 (p_f64 = 0; widened exactly to
+ *        float64 in registers, as pts64 = float64(pts32) in the reference)
+ *        or float64 (p_f64 = 1; lloyd_iterate's public float64 input);
+ * C64    (m, k, sub) float64 centroids, in/out;
+ * state  (m) int32: 1 = still iterating, 0 = stopped (the per-subspace
+ *        early stop of training.py:137-141 -- each subspace runs exactly the
+ *        iterations the reference's sequential loop would);
+ * workspace: cspq_lloyd_workspace_bytes() bytes of device memory,
+ *        zero-initialised once by the caller. */
+size_t cspq_lloyd_workspace_bytes(int64_t n, int32_t m, int32_t sub, int32_t k);
+
+/* Assignment step (training.py:57-73, _assign) for rows [row_begin, row_end)
+ * of every active subspace: assign (m, n) int32 = argmin_l ||c_l||^2 -
+ * 2 x.c_l in float64 (first index on ties), sq (m, n) float64 =
+ * max(d_min + ||x||^2, 0).  Row ranges let a multi-GPU run shard the
+ * assignment; rows outside the range are left untouched. */
+int cspq_lloyd_assign(const void *P, int32_t p_f64, int64_t n, int32_t m, int32_t sub, int32_t k,
+                      const double *C64, const int32_t *state, int64_t row_begin, int64_t row_end,
+                      int32_t *assign, double *sq, void *workspace, void *stream);
+
+/* Statistics of rows [row_begin, row_end) (training.py:73, 121-124):
+ * counts (m, k) float64 (np.bincount), sums (m, k, sub) float64 accumulated
+ * in ascending point order exactly like np.add.at (a stable counting sort by
+ * cluster, then one sequential chain per (cluster, coordinate)), and
+ * obj (m) float64 = numpy's pairwise sum of sq over the range.  With the
+ * full range these are the reference's bits (given identical assignments);
+ * sub-ranges give per-rank partials of a row-sharded run. */
+int cspq_lloyd_accumulate(const void *P, int32_t p_f64, int64_t n, int32_t m, int32_t sub, int32_t k,
+                          const int32_t *state, const int32_t *assign, const double *sq,
+                          int64_t row_begin, int64_t row_end, double *counts, double *sums,
+                          double *obj, void *workspace, void *stream);
+
+/* Mean update for non-empty clusters (training.py:125-126) and the list of
+ * empty clusters: empties (m, k) int32 gets the ascending empty ids,
+ * n_empty (m) int32 their number. */
+int cspq_lloyd_update(const double *counts, const double *sums, int32_t m, int32_t k,
+                      int32_t sub, const int32_t *state, double *C64, int32_t *empties,
+                      int32_t *n_empty, void *stream);
+
+/* Empty-cluster teleport (training.py:129-136): residual ||x - c_assign||^2
+ * against the updated centroids, then each empty cluster in ascending order
+ * takes the current argmax-residual point (ties -> smallest point index)
+ * and that residual is set to -1. */
+int cspq_lloyd_repair(const void *P, int32_t p_f64, int64_t n, int32_t m, int32_t sub, int32_t k,
+                      const int32_t *assign, const int32_t *state, const int32_t *empties,
+                      const int32_t *n_empty, double *C64, void *workspace, void *stream);
+
+/* Stop rule (training.py:137-141): record obj into
+ * objectives[j, iterations[j]], increment iterations[j], and stop subspace
+ * j if obj == 0 or prev - obj <= tol * max(prev, 1e-300) (or max_iters is
+ * reached).  prev (m) float64 starts at +inf; objectives is
+ * (m, max_iters + 1). */
+int cspq_lloyd_stop(const double *obj, int32_t m, int32_t max_iters, double tol, int32_t *state,
+                    double *prev, int32_t *iterations, double *objectives, void *stream);
+
+/* Whole single-device Lloyd run: max_iters x (assign, accumulate, update,
+ * repair, stop), then the float32 cast, the REFERENCE-variant final
+ * assignment of float32(points) and the final objective
+ * (training.py:143-154).  Outputs: C32 (m, k, sub) float32, assign (m, n)
+ * int32 (final pass), objectives (m, max_iters + 1) float64 with
+ * iterations[j] + 1 valid entries, iterations (m) int32. */
+int cspq_lloyd_train(const void *P, int32_t p_f64, int64_t n, int32_t m, int32_t sub, int32_t k,
+                     double *C64, int32_t max_iters, double tol, float *C32, int32_t *assign,
+                     double *objectives, int32_t *iterations, void *workspace, void *stream);
+
+/* Final objective of training.py:151-154: obj (m) = pairwise sum over
+ * points of ||x - float64(C32[assign])||^2. */
+int cspq_lloyd_final_objective(const void *P, int32_t p_f64, int64_t n, int32_t m, int32_t sub,
+                               int32_t k, const float *C32, const int32_t *assign, double *obj,
+                               void *workspace, void *stream);
+
+/* k-means++ seeding (training.py:76-92) for every subspace: C64[j, 0] =
+ * P[j, first[j]], then for c = 1..k-1 the reference's
+ * rng.choice(n, p = d2 / d2.sum()) -- cdf = cumsum(p) (sequential),
+ * cdf /= cdf[-1], searchsorted(cdf, u[j, c-1], 'right') -- and
+ * d2 = minimum(d2, ||x - c||^2).  first (m) int64 and u (m, k-1) float64
+ * are the host generator's draws (rng.integers(n), then one rng.random()
+ * per choice).  status (m) int32 = 2 if a step met zero total mass (the
+ * reference would have drawn rng.integers there instead). */
+int cspq_kmeanspp(const void *P, int32_t p_f64, int64_t n, int32_t m, int32_t sub, int32_t k,
+                  const int64_t *first, const double *u, double *C64, int32_t *status,
+                  void *workspace, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSPQ_B200_H */

@@ -1,0 +1,288 @@
+"""Dataset-scale encoding on the B200 -- the drop-in for ``cspq.bulk``.
+
+Reference: /root/reference/pkg/src/cspq/bulk.py:31-195.  The reference cuts
+the rows into ``block_size`` blocks and hands them round-robin to a thread
+pool of nogil numba drivers (bulk.py:139-155).  Here the whole matrix goes
+to one fused CUDA kernel (device-resident rows) or through the pipelined
+host->device->host path of the C ABI (host rows); the plan still validates
+exactly like the reference's, and -- as there -- never changes the codes.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from contextlib import contextmanager
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from ._device import device as _device, ptr, stream_ptr, to_device, torch
+from .core import Codebook, ConfigError, PQCodes, PQParams
+from .kernels import EncoderVariant, native_lane_width
+
+CHUNK_MAJOR = "chunk_major"
+VECTOR_MAJOR = "vector_major"
+
+_VARIANT_IDS = {
+    EncoderVariant.REFERENCE: N.VARIANT_REFERENCE,
+    EncoderVariant.REFORMULATED: N.VARIANT_REFORMULATED,
+    EncoderVariant.BLOCKED: N.VARIANT_BLOCKED,
+}
+_MODES = {"auto": N.MODE_AUTO, "exact": N.MODE_EXACT, "guarded": N.MODE_GUARDED}
+
+
+@dataclass(frozen=True)
+class ExecutionPlan:
+    """Scheduling knobs (bulk.py:31-50).  order / block_size / w / workers
+    are the reference's and are validated identically; on the GPU they are
+    performance-only (codes are plan-invariant, test_bulk.py:44-62).
+    GPU extras: ``mode`` ("auto" | "exact" | "guarded" -- all give the
+    oracle's codes), ``batch_rows`` (rows per host<->device batch; None =
+    max(block_size, 65536)), ``streams`` (CUDA streams in that pipeline) and
+    ``device`` (CUDA ordinal; None = current)."""
+
+    order: str = CHUNK_MAJOR
+    block_size: int = 4096
+    variant: EncoderVariant = EncoderVariant.BLOCKED
+    w: int | None = None
+    workers: int = 1
+    mode: str = "auto"
+    batch_rows: int | None = None
+    streams: int = 3
+    device: int | None = None
+
+    def __post_init__(self):
+        if self.order not in (CHUNK_MAJOR, VECTOR_MAJOR):
+            raise ConfigError(f"unknown order {self.order!r}")
+        if self.block_size < 1:
+            raise ConfigError(f"block_size must be >= 1, got {self.block_size}")
+        if self.workers < 1:
+            raise ConfigError(f"workers must be >= 1, got {self.workers}")
+        if self.w is not None and self.w < 1:
+            raise ConfigError(f"w must be >= 1, got {self.w}")
+        if self.mode not in _MODES:
+            raise ConfigError(f"unknown mode {self.mode!r}")
+        if self.batch_rows is not None and self.batch_rows < 1:
+            raise ConfigError(f"batch_rows must be >= 1, got {self.batch_rows}")
+        if not 1 <= self.streams <= 16:
+            raise ConfigError(f"streams must be in [1, 16], got {self.streams}")
+
+    def resolved_w(self) -> int:
+        return self.w if self.w is not None else native_lane_width()
+
+    def resolved_batch_rows(self) -> int:
+        return self.batch_rows if self.batch_rows is not None else max(self.block_size, 1 << 16)
+
+
+@dataclass(frozen=True)
+class CodebookSet:
+    """All m codebooks stacked (bulk.py:53-105): rowmajor (m, k, sub),
+    transposed (m, sub, k), biases (m, k), float32.  The device copy (and
+    the encode guard constants) is uploaded once per device and cached."""
+
+    rowmajor: np.ndarray
+    transposed: np.ndarray
+    biases: np.ndarray
+    _dev: dict = field(default_factory=dict, compare=False, repr=False)
+
+    @classmethod
+    def from_codebooks(cls, codebooks) -> "CodebookSet":
+        if isinstance(codebooks, cls):
+            return codebooks
+        cbs = list(codebooks)
+        if not cbs:
+            raise ConfigError("no codebooks given")
+        k, sub = cbs[0].k, cbs[0].sub_dim
+        if any(cb.k != k or cb.sub_dim != sub for cb in cbs):
+            raise ConfigError("codebooks disagree on sub_dim or k")
+        arrays = [np.ascontiguousarray(np.stack(a)) for a in (
+            [cb.centroids_rowmajor for cb in cbs],
+            [cb.centroids_transposed for cb in cbs],
+            [cb.biases for cb in cbs])]
+        for a in arrays:
+            a.flags.writeable = False
+        return cls(*arrays)
+
+    @property
+    def m(self) -> int:
+        return self.rowmajor.shape[0]
+
+    @property
+    def k(self) -> int:
+        return self.rowmajor.shape[1]
+
+    @property
+    def sub_dim(self) -> int:
+        return self.rowmajor.shape[2]
+
+    @property
+    def d(self) -> int:
+        return self.m * self.sub_dim
+
+    def __getitem__(self, j: int) -> Codebook:
+        return Codebook(j, self.rowmajor[j], self.transposed[j], self.biases[j])
+
+    def on_device(self, dev=None):
+        """(rowmajor, biases, guard, recomputed_biases) as CUDA tensors."""
+        dev = _device() if dev is None else dev
+        key = (dev.type, dev.index)
+        hit = self._dev.get(key)
+        if hit is None:
+            t = torch()
+            rm = to_device(self.rowmajor, dev, t.float32)
+            bs = to_device(self.biases, dev, t.float32)
+            guard = t.empty((self.m, 2), dtype=t.float32, device=dev)
+            nob = t.empty((self.m, self.k), dtype=t.float32, device=dev)
+            with t.cuda.device(dev):
+                sp = stream_ptr(dev)
+                N.call("cspq_encode_prepare", ptr(rm), ptr(bs), self.m, self.k, self.sub_dim, ptr(guard), sp)
+                N.call("cspq_recompute_biases_f32", ptr(rm), self.m, self.k, self.sub_dim, ptr(nob), sp)
+                guard_nob = t.empty((self.m, 2), dtype=t.float32, device=dev)
+                N.call("cspq_encode_prepare", ptr(rm), ptr(nob), self.m, self.k, self.sub_dim, ptr(guard_nob), sp)
+            hit = (rm, bs, guard, nob, guard_nob)
+            self._dev[key] = hit
+        return hit
+
+
+def _resolve_input(dataset):
+    """-> (array-or-tensor, is_cuda_tensor).  VectorDataset, numpy, torch."""
+    t = torch()
+    if isinstance(dataset, t.Tensor):
+        return dataset, dataset.is_cuda
+    X = dataset.data if isinstance(getattr(dataset, "data", None), np.ndarray) else dataset
+    return np.asarray(X), False
+
+
+def _variant_args(cbset: CodebookSet, plan: ExecutionPlan, precomputed_bias: bool, dev):
+    rm, bs, guard, nob, guard_nob = cbset.on_device(dev)
+    vid = _VARIANT_IDS[plan.variant]
+    if plan.variant is EncoderVariant.BLOCKED and not precomputed_bias:
+        # kernels.py:146-157: bias recomputed as 0.5f * fl-chain(c*c) -- a
+        # per-codebook constant, so one table gives the same bits
+        return rm, nob, guard_nob, vid
+    return rm, bs, guard, vid
+
+
+def encode_dataset_device(X, codebooks, plan: ExecutionPlan | None = None, *,
+                          precomputed_bias: bool = True, out=None):
+    """Encode a CUDA tensor X (n, d) float32/uint8 in place on its device;
+    returns the (n, m) codes tensor (uint8, or int16 holding uint16 bits
+    when k > 256).  Stream-ordered on the current stream, no sync."""
+    t = torch()
+    plan = plan or ExecutionPlan()
+    cbset = CodebookSet.from_codebooks(codebooks)
+    if X.dim() != 2:
+        raise ConfigError(f"dataset must be 2-D, got shape {tuple(X.shape)}")
+    if X.dtype not in (t.float32, t.uint8):
+        X = X.float()
+    if X.stride(1) != 1:
+        X = X.contiguous()
+    n, d = X.shape
+    dev = X.device
+    cdt = t.uint8 if cbset.k <= 256 else t.int16
+    if out is None:
+        out = t.empty((n, cbset.m), dtype=cdt, device=dev)
+    if n == 0:
+        return out
+    if d != cbset.d:
+        raise ConfigError(f"dataset dimensionality {d} does not match codebooks' d={cbset.d}")
+    rm, bs, guard, vid = _variant_args(cbset, plan, precomputed_bias, dev)
+    xrs = X.stride(0) if n > 1 else d  # a 1-row view may carry any row stride
+    with t.cuda.device(dev):
+        N.call("cspq_encode", ptr(X), N.IN_U8 if X.dtype == t.uint8 else N.IN_F32, n, d, xrs,
+               ptr(rm), ptr(bs), ptr(guard), cbset.m, cbset.k, cbset.sub_dim, ptr(out), out.stride(0),
+               vid, _MODES[plan.mode], stream_ptr(dev))
+    return out
+
+
+def encode_dataset_host(X: np.ndarray, codebooks, plan: ExecutionPlan | None = None, *,
+                        precomputed_bias: bool = True, out: np.ndarray | None = None,
+                        batch_ms: np.ndarray | None = None) -> np.ndarray:
+    """Encode host rows through the C ABI's pipelined H2D -> encode -> D2H path
+    (cspq_encode_host).  Pinned inputs/outputs (``pinned_empty``) are copied
+    directly; pageable ones are staged through a pinned ring."""
+    N.require_cuda()
+    plan = plan or ExecutionPlan()
+    cbset = CodebookSet.from_codebooks(codebooks)
+    in_u8 = X.dtype == np.uint8
+    if not in_u8:
+        X = np.ascontiguousarray(X, dtype=np.float32)
+    elif not X.flags.c_contiguous:
+        X = np.ascontiguousarray(X)
+    n, d = X.shape
+    cdt = np.uint8 if cbset.k <= 256 else np.uint16
+    if out is None:
+        out = np.empty((n, cbset.m), dtype=cdt)
+    if n == 0:
+        return out
+    if d != cbset.d:
+        raise ConfigError(f"dataset dimensionality {d} does not match codebooks' d={cbset.d}")
+    dev = _device(plan.device)
+    rm, bs, guard, vid = _variant_args(cbset, plan, precomputed_bias, dev)
+    t = torch()
+    t.cuda.current_stream(dev).synchronize()  # codebook upload visible to the pipeline streams
+    nb = -(-n // plan.resolved_batch_rows())
+    if batch_ms is not None and batch_ms.shape[0] < nb:
+        raise ConfigError("batch_ms too small")
+    N.call("cspq_encode_host", X.ctypes.data_as(ctypes.c_void_p), N.IN_U8 if in_u8 else N.IN_F32, n, d,
+           ptr(rm), ptr(bs), ptr(guard), cbset.m, cbset.k, cbset.sub_dim,
+           out.ctypes.data_as(ctypes.c_void_p), vid, _MODES[plan.mode], plan.resolved_batch_rows(),
+           plan.streams, None if batch_ms is None else batch_ms.ctypes.data_as(ctypes.c_void_p),
+           dev.index)
+    return out
+
+
+def encode_dataset(dataset, codebooks, plan: ExecutionPlan | None = None, *,
+                   precomputed_bias: bool = True) -> PQCodes:
+    """Encode every vector (bulk.py:108-157); the plan never changes codes.
+
+    Accepts a VectorDataset, a numpy array (float32, or uint8 widened
+    exactly in-kernel) or a torch tensor (CUDA tensors are encoded where
+    they live).  Returns host ``PQCodes`` like the reference; use
+    ``encode_dataset_device`` to keep codes on the GPU."""
+    plan = plan or ExecutionPlan()
+    cbset = CodebookSet.from_codebooks(codebooks)
+    X, on_gpu = _resolve_input(dataset)
+    if X.ndim != 2:
+        raise ConfigError(f"dataset must be 2-D, got shape {tuple(X.shape)}")
+    dtype = np.uint8 if cbset.k <= 256 else np.uint16
+    if X.shape[0] == 0:
+        return PQCodes(codes=np.empty((0, cbset.m), dtype=dtype), k=cbset.k)
+    if X.shape[1] != cbset.d:
+        raise ConfigError(f"dataset dimensionality {X.shape[1]} does not match codebooks' d={cbset.d}")
+    if on_gpu:
+        codes = encode_dataset_device(X, cbset, plan, precomputed_bias=precomputed_bias).cpu().numpy()
+        if dtype == np.uint16:
+            codes = codes.view(np.uint16)
+    else:
+        if not isinstance(X, np.ndarray):
+            X = X.numpy()
+        if X.dtype != np.uint8 and X.dtype != np.float32:
+            X = X.astype(np.float32)
+        codes = encode_dataset_host(X, cbset, plan, precomputed_bias=precomputed_bias)
+    return PQCodes(codes=codes, k=cbset.k)
+
+
+@contextmanager
+def kernel_allocation_probe(record: dict):
+    """Counterpart of bulk.py:160-184.  The reference counts numba heap
+    allocations per driver call; the CUDA kernels allocate nothing at all
+    (all scratch is registers/shared memory), so the probe reports the
+    torch caching-allocator's change in allocated device bytes."""
+    t = torch()
+    dev = t.cuda.current_device() if t.cuda.is_available() else None
+    start = t.cuda.memory_allocated(dev) if dev is not None else 0
+    try:
+        yield record
+    finally:
+        end = t.cuda.memory_allocated(dev) if dev is not None else 0
+        record["device_bytes"] = end - start
+
+
+def estimate_working_set(params: PQParams, plan: ExecutionPlan) -> int:
+    """Resident bytes during bulk encoding, independent of dataset size
+    (bulk.py:187-195): one codebook in both layouts plus biases, plus the
+    per-worker lane state."""
+    resident = 2 * params.k * params.sub_dim * 4 + params.k * 4
+    return resident + plan.workers * 2 * plan.resolved_w() * 4

@@ -1,0 +1,794 @@
+// lloyd.cu -- Lloyd k-means for all M subspaces at once, float64, sm_100a.
+//
+// Restates the reference's lloyd_iterate (/root/reference/pkg/src/cspq/
+// training.py:109-159) with its _assign (training.py:57-73), batched over
+// subspaces instead of the reference's sequential subspace loop
+// (training.py:212-223).  Arithmetic follows the oracle (oracle/pq_oracle.c)
+// operation for operation so GPU and oracle agree bit for bit:
+//   * assignment: ||c||^2 as a sequential mul-then-add sum, x.c as an
+//     ascending fused chain (a dgemm micro-kernel's rank-1 order),
+//     d = ||c||^2 - 2 x.c, argmin first index (np.argmin);
+//   * objective terms sq = np.maximum(d_min + ||x||^2, 0) and their sum in
+//     numpy's pairwise-summation tree (ndarray.sum);
+//   * counts (np.bincount) and sums accumulated in ascending point order,
+//     which is what np.add.at does: a stable counting sort by cluster
+//     (per-chunk histograms -> scan -> warp-stable scatter with
+//     __match_any_sync) followed by one sequential float64 chain per
+//     (cluster, coordinate).  No floating-point atomics anywhere, so the
+//     result is deterministic and equal to the reference's for identical
+//     assignments;
+//   * mean for non-empty clusters with IEEE division; empty clusters
+//     teleported (ascending) onto the argmax residual point (ties ->
+//     smallest index), that residual then set to -1;
+//   * stop rule obj == 0 or prev - obj <= tol * max(prev, 1e-300), kept per
+//     subspace (state[j]) so every subspace runs exactly the iterations the
+//     reference's sequential loop would.
+
+#include "common.cuh"
+
+namespace cspq {
+
+namespace {
+
+constexpr int kChunk = 1024;  // points per histogram/scatter chunk
+constexpr uint64_t kMagic = 0x43535051424C4C59ull;
+
+inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+struct WsLayout {
+    int64_t header, leaves, hist, cnt, start, perm, sq, resid, leafsum, cn;
+    // train-loop state
+    int64_t counts, sums, obj, prev, state, empties, nempty, assign_it;
+    // float32 copy of float64 points (final pass), k-means++ scratch
+    int64_t p32, d2, pp;
+    int64_t total;
+    int64_t nch, maxleaves;
+    WsLayout(int64_t n, int m, int sub, int k) {
+        nch = (n + kChunk - 1) / kChunk;
+        maxleaves = n / 32 + 8;
+        int64_t o = 0;
+        auto take = [&](int64_t bytes) { int64_t r = o; o = align_up(o + bytes, 256); return r; };
+        header = take(256);
+        leaves = take(16 * maxleaves);
+        hist = take(4 * (int64_t)m * nch * k);
+        cnt = take(4 * (int64_t)m * k);
+        start = take(4 * (int64_t)m * k);
+        perm = take(4 * (int64_t)m * n);
+        sq = take(8 * (int64_t)m * n);
+        resid = take(8 * (int64_t)m * n);
+        leafsum = take(8 * (int64_t)m * maxleaves);
+        cn = take(8 * (int64_t)m * k);
+        counts = take(8 * (int64_t)m * k);
+        sums = take(8 * (int64_t)m * k * sub);
+        obj = take(8 * (int64_t)m);
+        prev = take(8 * (int64_t)m);
+        state = take(4 * (int64_t)m);
+        empties = take(4 * (int64_t)m * k);
+        nempty = take(4 * (int64_t)m);
+        assign_it = take(4 * (int64_t)m * n);
+        p32 = take(4 * (int64_t)m * n * sub);
+        d2 = take(8 * (int64_t)m * n);
+        pp = take(8 * (int64_t)m * n);
+        total = o;
+    }
+    template <typename T>
+    T *at(void *ws, int64_t off) const { return reinterpret_cast<T *>(reinterpret_cast<char *>(ws) + off); }
+};
+
+struct WsHeader {
+    uint64_t magic;
+    int64_t leaves_for;  // range length the leaf table describes
+    int64_t nleaves;
+};
+
+// ---------------------------------------------------------------- pairwise tree
+// Leaves of numpy's pairwise summation of a length-n range, in order
+// (pairwise_sum: n <= 128 is a leaf; otherwise split at n2 = n/2 - (n/2)%8).
+__global__ void leaves_kernel(int64_t n, int64_t *leaves, WsHeader *hdr) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (hdr->magic == kMagic && hdr->leaves_for == n) return;
+    struct F { int64_t lo, len; };
+    F st[96];
+    int sp = 0;
+    int64_t nl = 0;
+    st[sp++] = {0, n};
+    while (sp) {
+        F f = st[--sp];
+        if (f.len <= 128) { leaves[2 * nl] = f.lo; leaves[2 * nl + 1] = f.len; ++nl; continue; }
+        int64_t n2 = f.len / 2;
+        n2 -= n2 % 8;
+        st[sp++] = {f.lo + n2, f.len - n2};  // right pushed first: left is visited first
+        st[sp++] = {f.lo, n2};
+    }
+    hdr->magic = kMagic;
+    hdr->leaves_for = n;
+    hdr->nleaves = nl;
+}
+
+// numpy leaf sum: <8 sequential from 0.0; else 8 accumulators, fixed combine, tail
+__device__ double leaf_sum(const double *a, int64_t n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+        return r;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+}
+
+// leafsum[j][l] for values vals[j*vstride + lo .. ]
+__global__ void leafsum_kernel(const double *vals, int64_t vstride, int64_t begin, int m,
+                               const int32_t *state, const int64_t *leaves, const WsHeader *hdr,
+                               int64_t maxleaves, double *leafsum) {
+    const int64_t nl = hdr->nleaves;
+    const int j = blockIdx.y;
+    if (state && !state[j]) return;
+    for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < nl; l += (int64_t)gridDim.x * blockDim.x)
+        leafsum[(int64_t)j * maxleaves + l] = leaf_sum(vals + (int64_t)j * vstride + begin + leaves[2 * l], leaves[2 * l + 1]);
+}
+
+// recombine leaves along the same recursion (one thread per subspace)
+__global__ void combine_kernel(int64_t n, int m, const int32_t *state, const double *leafsum,
+                               int64_t maxleaves, double *out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    if (state && !state[j]) return;
+    const double *ls = leafsum + (int64_t)j * maxleaves;
+    struct F { int64_t len, n2; int stage; double left; };
+    F st[96];
+    int sp = 0;
+    int64_t leaf = 0;
+    double ret = 0.0;
+    st[0] = {n, 0, 0, 0.0};
+    for (;;) {
+        F &f = st[sp];
+        if (f.stage == 0) {
+            if (f.len <= 128) {
+                ret = ls[leaf++];
+                if (sp == 0) break;
+                --sp;
+                continue;
+            }
+            int64_t n2 = f.len / 2;
+            n2 -= n2 % 8;
+            f.n2 = n2;
+            f.stage = 1;
+            st[++sp] = {n2, 0, 0, 0.0};
+        } else if (f.stage == 1) {
+            f.left = ret;
+            f.stage = 2;
+            const int64_t rl = f.len - f.n2;
+            st[++sp] = {rl, 0, 0, 0.0};
+        } else {
+            ret = __dadd_rn(f.left, ret);
+            if (sp == 0) break;
+            --sp;
+        }
+    }
+    out[j] = ret;
+}
+
+// ---------------------------------------------------------------- assignment
+__global__ void cnorm_kernel(const double *C64, int m, int k, int sub, const int32_t *state, double *cn) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)m * k) return;
+    const int j = (int)(i / k);
+    if (state && !state[j]) return;
+    const double *c = C64 + i * sub;
+    double s = 0.0;
+    for (int t = 0; t < sub; ++t) s = __dadd_rn(s, __dmul_rn(c[t], c[t]));
+    cn[i] = s;
+}
+
+template <int SUBC, typename TP>
+__global__ void __launch_bounds__(256)
+assign_kernel(const TP *__restrict__ P, int64_t n, int k, int sub_rt, const double *__restrict__ C64,
+              const double *__restrict__ cn_g, const int32_t *__restrict__ state, int64_t b, int64_t e,
+              int32_t *__restrict__ assign, double *__restrict__ sq, int use_smem) {
+    const int sub = SUBC > 0 ? SUBC : sub_rt;
+    const int j = blockIdx.y;
+    if (!state[j]) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const double *Cj = C64 + (int64_t)j * k * sub;
+    const double *cnj = cn_g + (int64_t)j * k;
+    if (use_smem) {
+        double *sC = reinterpret_cast<double *>(smem_raw);
+        double *scn = sC + (int64_t)k * sub;
+        for (int q = threadIdx.x; q < k * sub; q += blockDim.x) sC[q] = Cj[q];
+        for (int q = threadIdx.x; q < k; q += blockDim.x) scn[q] = cnj[q];
+        __syncthreads();
+        Cj = sC;
+        cnj = scn;
+    }
+    const TP *Pj = P + (int64_t)j * n * sub;
+    for (int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
+        double best = 0.0;
+        int bi = 0;
+        double xx = 0.0;
+        if constexpr (SUBC > 0) {
+            double x[SUBC];
+#pragma unroll
+            for (int t = 0; t < SUBC; ++t) x[t] = (double)Pj[i * SUBC + t];
+            for (int l = 0; l < k; ++l) {
+                const double *c = Cj + (int64_t)l * SUBC;
+                double dot = 0.0;
+#pragma unroll
+                for (int t = 0; t < SUBC; ++t) dot = __fma_rn(x[t], c[t], dot);
+                const double dl = __dsub_rn(cnj[l], __dmul_rn(2.0, dot));
+                if (l == 0 || dl < best) { best = dl; bi = l; }
+            }
+#pragma unroll
+            for (int t = 0; t < SUBC; ++t) xx = __dadd_rn(xx, __dmul_rn(x[t], x[t]));
+        } else {
+            const TP *x = Pj + i * sub;
+            for (int l = 0; l < k; ++l) {
+                const double *c = Cj + (int64_t)l * sub;
+                double dot = 0.0;
+                for (int t = 0; t < sub; ++t) dot = __fma_rn((double)x[t], c[t], dot);
+                const double dl = __dsub_rn(cnj[l], __dmul_rn(2.0, dot));
+                if (l == 0 || dl < best) { best = dl; bi = l; }
+            }
+            for (int t = 0; t < sub; ++t) xx = __dadd_rn(xx, __dmul_rn((double)x[t], (double)x[t]));
+        }
+        const double v = __dadd_rn(best, xx);
+        assign[(int64_t)j * n + i] = bi;
+        sq[(int64_t)j * n + i] = (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(v, 0.0)
+    }
+}
+
+// ---------------------------------------------------------------- counting sort
+__global__ void hist_kernel(const int32_t *__restrict__ assign, int64_t n, int k, const int32_t *state,
+                            int64_t b, int64_t e, int64_t nch, int32_t *__restrict__ hist, int use_smem) {
+    const int j = blockIdx.y;
+    if (!state[j]) return;
+    const int64_t c = blockIdx.x;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int32_t *h = use_smem ? reinterpret_cast<int32_t *>(smem_raw) : hist + ((int64_t)j * nch + c) * k;
+    for (int q = threadIdx.x; q < k; q += blockDim.x) h[q] = 0;
+    __syncthreads();
+    const int64_t lo = b + c * kChunk, hi = min(e, lo + kChunk);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&h[assign[(int64_t)j * n + i]], 1);
+    __syncthreads();
+    if (use_smem)
+        for (int q = threadIdx.x; q < k; q += blockDim.x) hist[((int64_t)j * nch + c) * k + q] = h[q];
+}
+
+// per bin: chunk offsets (in place), counts; then bin starts
+__global__ void scan_kernel(int32_t *__restrict__ hist, int k, int64_t nch, const int32_t *state,
+                            int32_t *__restrict__ cnt, int32_t *__restrict__ start, double *__restrict__ counts) {
+    const int j = blockIdx.x;
+    if (!state[j]) return;
+    int32_t *H = hist + (int64_t)j * nch * k;
+    for (int l = threadIdx.x; l < k; l += blockDim.x) {
+        int32_t run = 0;
+        for (int64_t c = 0; c < nch; ++c) {
+            const int32_t v = H[c * k + l];
+            H[c * k + l] = run;
+            run += v;
+        }
+        cnt[(int64_t)j * k + l] = run;
+        counts[(int64_t)j * k + l] = (double)run;
+    }
+    __syncthreads();
+    // exclusive scan of cnt over bins (block-wide, tiles of blockDim)
+    __shared__ int32_t s[1024];
+    __shared__ int32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < k; base += blockDim.x) {
+        const int l = base + threadIdx.x;
+        const int32_t v = l < k ? cnt[(int64_t)j * k + l] : 0;
+        s[threadIdx.x] = v;
+        __syncthreads();
+        for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+            const int32_t add = threadIdx.x >= (unsigned)off ? s[threadIdx.x - off] : 0;
+            __syncthreads();
+            s[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (l < k) start[(int64_t)j * k + l] = carry + s[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += s[threadIdx.x];
+        __syncthreads();
+    }
+    for (int l = threadIdx.x; l < k; l += blockDim.x) {
+        const int32_t st = start[(int64_t)j * k + l];
+        for (int64_t c = 0; c < nch; ++c) H[c * k + l] += st;
+    }
+}
+
+// stable scatter: perm[j][pos] = i, in ascending i within each cluster
+__global__ void scatter_kernel(const int32_t *__restrict__ assign, int64_t n, int k, const int32_t *state,
+                               int64_t b, int64_t e, int64_t nch, int32_t *__restrict__ hist,
+                               int32_t *__restrict__ perm) {
+    const int j = blockIdx.y;
+    if (!state[j]) return;
+    const int64_t c = blockIdx.x;
+    const int lane = threadIdx.x;
+    int32_t *run = hist + ((int64_t)j * nch + c) * k;
+    const int64_t lo = b + c * kChunk, hi = min(e, lo + kChunk);
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t base = lo; base < hi; base += 32) {
+        const int64_t i = base + lane;
+        const int a = i < hi ? assign[(int64_t)j * n + i] : -1 - lane;  // unique sentinels never match
+        const unsigned peers = __match_any_sync(0xffffffffu, a);
+        if (a >= 0) {
+            const int rank = __popc(peers & lt);
+            const int32_t pos = run[a] + rank;
+            perm[(int64_t)j * n + pos] = (int32_t)(i - b);
+        }
+        __syncwarp();
+        if (a >= 0 && lane == __ffs(peers) - 1) run[a] += __popc(peers);
+        __syncwarp();
+    }
+}
+
+// sums[j][l][t] = sequential float64 chain over the cluster's points (ascending i)
+template <int SUBC, typename TP>
+__global__ void sums_kernel(const TP *__restrict__ P, int64_t n, int m, int k, int sub_rt,
+                            const int32_t *state, int64_t b, const int32_t *__restrict__ cnt,
+                            const int32_t *__restrict__ start, const int32_t *__restrict__ perm,
+                            double *__restrict__ sums) {
+    const int sub = SUBC > 0 ? SUBC : sub_rt;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)m * k * sub) return;
+    const int t = (int)(g % sub);
+    const int64_t jl = g / sub;
+    const int j = (int)(jl / k);
+    if (!state[j]) return;
+    const int32_t c0 = start[jl], cc = cnt[jl];
+    const int32_t *pp = perm + (int64_t)j * n + c0;
+    const TP *Pj = P + ((int64_t)j * n + b) * sub + t;
+    double s = 0.0;
+    int32_t p = 0;
+    for (; p + 8 <= cc; p += 8) {
+        TP v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = Pj[(int64_t)pp[p + q] * sub];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s = __dadd_rn(s, (double)v[q]);
+    }
+    for (; p < cc; ++p) s = __dadd_rn(s, (double)Pj[(int64_t)pp[p] * sub]);
+    sums[g] = s;
+}
+
+// ---------------------------------------------------------------- update / repair / stop
+__global__ void update_kernel(const double *__restrict__ counts, const double *__restrict__ sums, int k,
+                              int sub, const int32_t *state, double *__restrict__ C64,
+                              int32_t *__restrict__ empties, int32_t *__restrict__ nempty) {
+    const int j = blockIdx.x;
+    if (!state[j]) return;
+    __shared__ int32_t s[1024];
+    __shared__ int32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < k; base += blockDim.x) {
+        const int l = base + threadIdx.x;
+        int flag = 0;
+        if (l < k) {
+            const double cntv = counts[(int64_t)j * k + l];
+            if (cntv > 0) {
+                for (int t = 0; t < sub; ++t) {
+                    const int64_t q = ((int64_t)j * k + l) * sub + t;
+                    C64[q] = __ddiv_rn(sums[q], cntv);
+                }
+            } else {
+                flag = 1;
+            }
+        }
+        s[threadIdx.x] = flag;
+        __syncthreads();
+        for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+            const int32_t add = threadIdx.x >= (unsigned)off ? s[threadIdx.x - off] : 0;
+            __syncthreads();
+            s[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (flag) empties[(int64_t)j * k + carry + s[threadIdx.x] - 1] = l;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += s[threadIdx.x];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) nempty[j] = carry;
+}
+
+template <typename TP>
+__global__ void __launch_bounds__(1024)
+repair_kernel(const TP *__restrict__ P, int64_t n, int k, int sub, const int32_t *__restrict__ assign,
+              const int32_t *state, const int32_t *__restrict__ empties, const int32_t *__restrict__ nempty,
+              double *__restrict__ C64, double *__restrict__ resid) {
+    const int j = blockIdx.x;
+    if (!state[j] || nempty[j] == 0) return;
+    const TP *Pj = P + (int64_t)j * n * sub;
+    double *C = C64 + (int64_t)j * k * sub;
+    double *R = resid + (int64_t)j * n;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double *c = C + (int64_t)assign[(int64_t)j * n + i] * sub;
+        double r = 0.0;
+        for (int t = 0; t < sub; ++t) {
+            const double df = __dsub_rn((double)Pj[i * sub + t], c[t]);
+            r = __dadd_rn(r, __dmul_rn(df, df));
+        }
+        R[i] = r;
+    }
+    __syncthreads();
+    __shared__ double sv[1024];
+    __shared__ int64_t si[1024];
+    const int ne = nempty[j];
+    for (int q = 0; q < ne; ++q) {
+        double bv = -pos_inf_d();
+        int64_t bi = -1;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const double v = R[i];
+            if (bi < 0 || v > bv) { bv = v; bi = i; }  // ascending i per thread: first max kept
+        }
+        sv[threadIdx.x] = bv;
+        si[threadIdx.x] = bi;
+        __syncthreads();
+        for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+            if (threadIdx.x < (unsigned)off) {
+                const double ov = sv[threadIdx.x + off];
+                const int64_t oi = si[threadIdx.x + off];
+                const double mv = sv[threadIdx.x];
+                const int64_t mi = si[threadIdx.x];
+                if (oi >= 0 && (mi < 0 || ov > mv || (ov == mv && oi < mi))) {
+                    sv[threadIdx.x] = ov;
+                    si[threadIdx.x] = oi;
+                }
+            }
+            __syncthreads();
+        }
+        const int64_t cand = si[0];
+        const int e = empties[(int64_t)j * k + q];
+        if (threadIdx.x < (unsigned)sub) C[(int64_t)e * sub + threadIdx.x] = (double)Pj[cand * sub + threadIdx.x];
+        __syncthreads();
+        if (threadIdx.x == 0) R[cand] = -1.0;
+        __syncthreads();
+    }
+}
+
+__global__ void stop_kernel(const double *obj, int m, int max_iters, double tol, int32_t *state,
+                            double *prev, int32_t *iterations, double *objectives) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+        if (!state[j]) continue;
+        const double o = obj[j];
+        objectives[(int64_t)j * (max_iters + 1) + iterations[j]] = o;
+        iterations[j] += 1;
+        const double p = prev[j];
+        bool stop = (o == 0.0);
+        if (!stop && p < pos_inf_d()) {
+            const double scale = p > 1e-300 ? p : 1e-300;
+            stop = (p - o) <= tol * scale;
+        }
+        prev[j] = o;
+        if (stop || iterations[j] >= max_iters) state[j] = 0;
+    }
+}
+
+__global__ void init_state_kernel(int m, int32_t *state, double *prev, int32_t *iterations) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+        state[j] = 1;
+        prev[j] = pos_inf_d();
+        iterations[j] = 0;
+    }
+}
+
+__global__ void cast_kernel(const double *C64, int64_t tot, float *C32) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < tot) C32[i] = __double2float_rn(C64[i]);
+}
+
+template <typename TP>
+__global__ void final_resid_kernel(const TP *__restrict__ P, int64_t n, int k, int sub,
+                                   const float *__restrict__ C32, const int32_t *__restrict__ assign,
+                                   double *__restrict__ out) {
+    const int j = blockIdx.y;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const TP *x = P + ((int64_t)j * n + i) * sub;
+        const float *c = C32 + ((int64_t)j * k + assign[(int64_t)j * n + i]) * sub;
+        double r = 0.0;
+        for (int t = 0; t < sub; ++t) {
+            const double df = __dsub_rn((double)x[t], (double)c[t]);
+            r = __dadd_rn(r, __dmul_rn(df, df));
+        }
+        out[(int64_t)j * n + i] = r;
+    }
+}
+
+__global__ void write_final_obj_kernel(const double *obj, int m, int max_iters, const int32_t *iterations,
+                                       double *objectives) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x)
+        objectives[(int64_t)j * (max_iters + 1) + iterations[j]] = obj[j];
+}
+
+// ---------------------------------------------------------------- k-means++ (training.py:76-92)
+// d2[i] = ||x_i - c||^2 (diff then sequential mul-add, like the oracle), or
+// min(d2[i], that) (np.minimum(d2, ., out=d2)).
+template <typename TP>
+__global__ void kpp_dist_kernel(const TP *__restrict__ P, int64_t n, int sub, const double *__restrict__ C64,
+                                int k, int c, const int32_t *__restrict__ status, double *__restrict__ d2, int first) {
+    const int j = blockIdx.y;
+    if (status[j]) return;
+    const double *cen = C64 + ((int64_t)j * k + c) * sub;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const TP *x = P + ((int64_t)j * n + i) * sub;
+        double r = 0.0;
+        for (int t = 0; t < sub; ++t) {
+            const double df = __dsub_rn((double)x[t], cen[t]);
+            r = __dadd_rn(r, __dmul_rn(df, df));
+        }
+        double *o = d2 + (int64_t)j * n + i;
+        if (first) *o = r;
+        else {
+            const double cur = *o;
+            *o = (cur != cur || r != r) ? (cur != cur ? cur : r) : (r < cur ? r : cur);
+        }
+    }
+}
+
+// p = d2 / total (np: p = d2 / total)
+__global__ void kpp_div_kernel(const double *__restrict__ d2, int64_t n, const double *__restrict__ total,
+                               const int32_t *__restrict__ status, double *__restrict__ pp) {
+    const int j = blockIdx.y;
+    if (status[j]) return;
+    const double tot = total[j];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        pp[(int64_t)j * n + i] = __ddiv_rn(d2[(int64_t)j * n + i], tot);
+}
+
+// rng.choice(n, p=p): cdf = cumsum(p) (sequential); cdf /= cdf[-1];
+// idx = searchsorted(cdf, u, 'right').  One thread per subspace runs the
+// chain in place, then binary-searches the normalised (monotone) cdf.
+__global__ void kpp_choose_kernel(double *__restrict__ pp, int64_t n, int m, int k, int c,
+                                  const double *__restrict__ total, const double *__restrict__ u,
+                                  int32_t *__restrict__ status, const void *P, int pf64, int sub,
+                                  double *__restrict__ C64) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m || status[j]) return;
+    if (!(total[j] > 0.0)) { status[j] = 2; return; }  // all mass on chosen points
+    double *cdf = pp + (int64_t)j * n;
+    double run = 0.0;
+    for (int64_t i = 0; i < n; ++i) { run = __dadd_rn(run, cdf[i]); cdf[i] = run; }
+    const double last = run;
+    const double uu = u[(int64_t)j * (k - 1) + (c - 1)];
+    int64_t lo = 0, hi = n;  // first i with cdf[i]/last > uu
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ddiv_rn(cdf[mid], last) > uu) hi = mid; else lo = mid + 1;
+    }
+    int64_t idx = lo < n ? lo : n - 1;  // u < 1 and cdf[-1]/last == 1 keep lo < n
+    double *dst = C64 + ((int64_t)j * k + c) * sub;
+    for (int t = 0; t < sub; ++t)
+        dst[t] = pf64 ? reinterpret_cast<const double *>(P)[((int64_t)j * n + idx) * sub + t]
+                      : (double)reinterpret_cast<const float *>(P)[((int64_t)j * n + idx) * sub + t];
+}
+
+template <typename TP>
+__global__ void kpp_first_kernel(const TP *__restrict__ P, int64_t n, int m, int sub, int k,
+                                 const int64_t *__restrict__ first, double *__restrict__ C64, int32_t *status) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    status[j] = 0;
+    for (int t = 0; t < sub; ++t) C64[(int64_t)j * k * sub + t] = (double)P[((int64_t)j * n + first[j]) * sub + t];
+}
+
+template <typename TP>
+__global__ void cast_points_kernel(const TP *P, int64_t tot, float *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < tot) out[i] = (float)P[i];
+}
+
+int grid_for(int64_t items, int threads, int64_t cap = 148 * 16) {
+    int64_t g = (items + threads - 1) / threads;
+    if (g < 1) g = 1;
+    return (int)(g < cap ? g : cap);
+}
+
+// pairwise objective of vals[j][begin .. begin+len) for every active subspace
+int pairwise_obj(const double *vals, int64_t vstride, int64_t begin, int64_t len, int m,
+                 const int32_t *state, void *ws, const WsLayout &L, double *out, cudaStream_t st) {
+    WsHeader *hdr = L.at<WsHeader>(ws, L.header);
+    int64_t *leaves = L.at<int64_t>(ws, L.leaves);
+    double *leafsum = L.at<double>(ws, L.leafsum);
+    leaves_kernel<<<1, 1, 0, st>>>(len, leaves, hdr);
+    CSPQ_LAUNCH_CHECK();
+    const int64_t maxl = len / 32 + 8;
+    dim3 g((unsigned)grid_for(maxl, 128, 64), (unsigned)m);
+    leafsum_kernel<<<g, 128, 0, st>>>(vals, vstride, begin, m, state, leaves, hdr, L.maxleaves, leafsum);
+    CSPQ_LAUNCH_CHECK();
+    combine_kernel<<<(m + 63) / 64, 64, 0, st>>>(len, m, state, leafsum, L.maxleaves, out);
+    CSPQ_LAUNCH_CHECK();
+    return CSPQ_OK;
+}
+
+}  // namespace
+
+size_t lloyd_workspace_bytes(int64_t n, int m, int sub, int k) { return (size_t)WsLayout(n, m, sub, k).total; }
+
+#define CSPQ_TP_DISPATCH(pf64, P, ...)                                                                  \
+    do {                                                                                               \
+        if (pf64) { using TP = double; const TP *Pt = reinterpret_cast<const TP *>(P); __VA_ARGS__; } \
+        else { using TP = float; const TP *Pt = reinterpret_cast<const TP *>(P); __VA_ARGS__; }       \
+    } while (0)
+
+int lloyd_assign(const void *P, int pf64, int64_t n, int m, int sub, int k, const double *C64,
+                 const int32_t *state, int64_t b, int64_t e, int32_t *assign, double *sq, void *ws, cudaStream_t st) {
+    WsLayout L(n, m, sub, k);
+    double *cn = L.at<double>(ws, L.cn);
+    const int64_t mk = (int64_t)m * k;
+    cnorm_kernel<<<(unsigned)((mk + 255) / 256), 256, 0, st>>>(C64, m, k, sub, state, cn);
+    CSPQ_LAUNCH_CHECK();
+    if (e <= b) return CSPQ_OK;
+    const size_t need = (size_t)k * (sub + 1) * sizeof(double);
+    const int use_smem = need <= 96 * 1024;
+    const size_t smem = use_smem ? need : 0;
+    dim3 grid((unsigned)grid_for(e - b, 256, 148 * 8), (unsigned)m);
+    CSPQ_TP_DISPATCH(pf64, P, {
+        if (sub == 8) {
+            CSPQ_CUDA_TRY(cudaFuncSetAttribute(assign_kernel<8, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+            assign_kernel<8, TP><<<grid, 256, smem, st>>>(Pt, n, k, sub, C64, cn, state, b, e, assign, sq, use_smem);
+        } else if (sub == 4) {
+            CSPQ_CUDA_TRY(cudaFuncSetAttribute(assign_kernel<4, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+            assign_kernel<4, TP><<<grid, 256, smem, st>>>(Pt, n, k, sub, C64, cn, state, b, e, assign, sq, use_smem);
+        } else {
+            CSPQ_CUDA_TRY(cudaFuncSetAttribute(assign_kernel<0, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+            assign_kernel<0, TP><<<grid, 256, smem, st>>>(Pt, n, k, sub, C64, cn, state, b, e, assign, sq, use_smem);
+        }
+    });
+    CSPQ_LAUNCH_CHECK();
+    return CSPQ_OK;
+}
+
+int lloyd_accumulate(const void *P, int pf64, int64_t n, int m, int sub, int k, const int32_t *state,
+                     const int32_t *assign, const double *sq, int64_t b, int64_t e, double *counts,
+                     double *sums, double *obj, void *ws, cudaStream_t st) {
+    WsLayout L(n, m, sub, k);
+    const int64_t len = e - b;
+    const int64_t nch = (len + kChunk - 1) / kChunk;
+    int32_t *hist = L.at<int32_t>(ws, L.hist);
+    int32_t *cnt = L.at<int32_t>(ws, L.cnt);
+    int32_t *start = L.at<int32_t>(ws, L.start);
+    int32_t *perm = L.at<int32_t>(ws, L.perm);
+    if (nch > 0) {
+        const int use_smem = (size_t)k * 4 <= 48 * 1024;
+        hist_kernel<<<dim3((unsigned)nch, (unsigned)m), 256, use_smem ? k * 4 : 0, st>>>(assign, n, k, state, b, e, nch, hist, use_smem);
+        CSPQ_LAUNCH_CHECK();
+    }
+    scan_kernel<<<m, 256, 0, st>>>(hist, k, nch, state, cnt, start, counts);
+    CSPQ_LAUNCH_CHECK();
+    if (nch > 0) {
+        scatter_kernel<<<dim3((unsigned)nch, (unsigned)m), 32, 0, st>>>(assign, n, k, state, b, e, nch, hist, perm);
+        CSPQ_LAUNCH_CHECK();
+    }
+    const int64_t tot = (int64_t)m * k * sub;
+    const unsigned g = (unsigned)((tot + 127) / 128);
+    CSPQ_TP_DISPATCH(pf64, P, {
+        if (sub == 8) sums_kernel<8, TP><<<g, 128, 0, st>>>(Pt, n, m, k, sub, state, b, cnt, start, perm, sums);
+        else if (sub == 4) sums_kernel<4, TP><<<g, 128, 0, st>>>(Pt, n, m, k, sub, state, b, cnt, start, perm, sums);
+        else sums_kernel<0, TP><<<g, 128, 0, st>>>(Pt, n, m, k, sub, state, b, cnt, start, perm, sums);
+    });
+    CSPQ_LAUNCH_CHECK();
+    return pairwise_obj(sq, n, b, len, m, state, ws, L, obj, st);
+}
+
+int lloyd_update(const double *counts, const double *sums, int m, int k, int sub, const int32_t *state,
+                 double *C64, int32_t *empties, int32_t *nempty, cudaStream_t st) {
+    update_kernel<<<m, 256, 0, st>>>(counts, sums, k, sub, state, C64, empties, nempty);
+    CSPQ_LAUNCH_CHECK();
+    return CSPQ_OK;
+}
+
+int lloyd_repair(const void *P, int pf64, int64_t n, int m, int sub, int k, const int32_t *assign,
+                 const int32_t *state, const int32_t *empties, const int32_t *nempty, double *C64, void *ws,
+                 cudaStream_t st) {
+    WsLayout L(n, m, sub, k);
+    CSPQ_TP_DISPATCH(pf64, P, {
+        repair_kernel<TP><<<m, 1024, 0, st>>>(Pt, n, k, sub, assign, state, empties, nempty, C64, L.at<double>(ws, L.resid));
+    });
+    CSPQ_LAUNCH_CHECK();
+    return CSPQ_OK;
+}
+
+int lloyd_stop(const double *obj, int m, int max_iters, double tol, int32_t *state, double *prev,
+               int32_t *iterations, double *objectives, cudaStream_t st) {
+    stop_kernel<<<(m + 127) / 128, 128, 0, st>>>(obj, m, max_iters, tol, state, prev, iterations, objectives);
+    CSPQ_LAUNCH_CHECK();
+    return CSPQ_OK;
+}
+
+int encode_subspace_major(const float *P, int64_t n, int m, int sub, const float *CB, const float *B, int k,
+                          int32_t *assign, int variant, cudaStream_t st);
+
+int lloyd_final_objective(const void *P, int pf64, int64_t n, int m, int sub, int k, const float *C32,
+                          const int32_t *assign, double *obj, void *ws, cudaStream_t st) {
+    WsLayout L(n, m, sub, k);
+    double *r = L.at<double>(ws, L.resid);
+    dim3 g((unsigned)grid_for(n, 256, 256), (unsigned)m);
+    CSPQ_TP_DISPATCH(pf64, P, { final_resid_kernel<TP><<<g, 256, 0, st>>>(Pt, n, k, sub, C32, assign, r); });
+    CSPQ_LAUNCH_CHECK();
+    return pairwise_obj(r, n, 0, n, m, nullptr, ws, L, obj, st);
+}
+
+int lloyd_train(const void *P, int pf64, int64_t n, int m, int sub, int k, double *C64, int max_iters, double tol,
+                float *C32, int32_t *assign, double *objectives, int32_t *iterations, void *ws, cudaStream_t st) {
+    WsLayout L(n, m, sub, k);
+    int32_t *state = L.at<int32_t>(ws, L.state);
+    double *prev = L.at<double>(ws, L.prev);
+    double *sq = L.at<double>(ws, L.sq);
+    double *counts = L.at<double>(ws, L.counts);
+    double *sums = L.at<double>(ws, L.sums);
+    double *obj = L.at<double>(ws, L.obj);
+    int32_t *empties = L.at<int32_t>(ws, L.empties);
+    int32_t *nempty = L.at<int32_t>(ws, L.nempty);
+    int32_t *asg = L.at<int32_t>(ws, L.assign_it);
+    init_state_kernel<<<(m + 127) / 128, 128, 0, st>>>(m, state, prev, iterations);
+    CSPQ_LAUNCH_CHECK();
+    int rc;
+    for (int it = 0; it < max_iters; ++it) {
+        if ((rc = lloyd_assign(P, pf64, n, m, sub, k, C64, state, 0, n, asg, sq, ws, st))) return rc;
+        if ((rc = lloyd_accumulate(P, pf64, n, m, sub, k, state, asg, sq, 0, n, counts, sums, obj, ws, st))) return rc;
+        if ((rc = lloyd_update(counts, sums, m, k, sub, state, C64, empties, nempty, st))) return rc;
+        if ((rc = lloyd_repair(P, pf64, n, m, sub, k, asg, state, empties, nempty, C64, ws, st))) return rc;
+        if ((rc = lloyd_stop(obj, m, max_iters, tol, state, prev, iterations, objectives, st))) return rc;
+    }
+    const int64_t tot = (int64_t)m * k * sub;
+    cast_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(C64, tot, C32);
+    CSPQ_LAUNCH_CHECK();
+    // final pass with the float32 REFERENCE encoder on float32(points) (training.py:143-150)
+    const float *P32 = reinterpret_cast<const float *>(P);
+    if (pf64) {
+        float *p32 = L.at<float>(ws, L.p32);
+        const int64_t np = (int64_t)m * n * sub;
+        cast_points_kernel<double><<<(unsigned)((np + 255) / 256), 256, 0, st>>>(reinterpret_cast<const double *>(P), np, p32);
+        CSPQ_LAUNCH_CHECK();
+        P32 = p32;
+    }
+    if ((rc = encode_subspace_major(P32, n, m, sub, C32, nullptr, k, assign, CSPQ_VARIANT_REFERENCE, st))) return rc;
+    if ((rc = lloyd_final_objective(P, pf64, n, m, sub, k, C32, assign, obj, ws, st))) return rc;
+    write_final_obj_kernel<<<(m + 127) / 128, 128, 0, st>>>(obj, m, max_iters, iterations, objectives);
+    CSPQ_LAUNCH_CHECK();
+    return CSPQ_OK;
+}
+
+// k-means++ seeding for every subspace (training.py:76-92).  first (m) and
+// u (m, k-1) are the host RNG draws (rng.integers(n), then one rng.random()
+// per rng.choice).  status[j] = 2 if a step found zero total mass (the
+// reference would then draw rng.integers instead -- reported to the host).
+int kmeanspp(const void *P, int pf64, int64_t n, int m, int sub, int k, const int64_t *first, const double *u,
+             double *C64, int32_t *status, void *ws, cudaStream_t st) {
+    WsLayout L(n, m, sub, k);
+    double *d2 = L.at<double>(ws, L.d2);
+    double *pp = L.at<double>(ws, L.pp);
+    double *total = L.at<double>(ws, L.obj);
+    dim3 g((unsigned)grid_for(n, 256, 512), (unsigned)m);
+    int rc;
+    CSPQ_TP_DISPATCH(pf64, P, {
+        kpp_first_kernel<TP><<<(m + 63) / 64, 64, 0, st>>>(Pt, n, m, sub, k, first, C64, status);
+        CSPQ_LAUNCH_CHECK();
+        kpp_dist_kernel<TP><<<g, 256, 0, st>>>(Pt, n, sub, C64, k, 0, status, d2, 1);
+        CSPQ_LAUNCH_CHECK();
+        for (int c = 1; c < k; ++c) {
+            // status doubles as the "active" mask of pairwise_obj: 0 -> active
+            if ((rc = pairwise_obj(d2, n, 0, n, m, nullptr, ws, L, total, st))) return rc;
+            kpp_div_kernel<<<g, 256, 0, st>>>(d2, n, total, status, pp);
+            CSPQ_LAUNCH_CHECK();
+            kpp_choose_kernel<<<(m + 31) / 32, 32, 0, st>>>(pp, n, m, k, c, total, u, status, P, pf64, sub, C64);
+            CSPQ_LAUNCH_CHECK();
+            kpp_dist_kernel<TP><<<g, 256, 0, st>>>(Pt, n, sub, C64, k, c, status, d2, 0);
+            CSPQ_LAUNCH_CHECK();
+        }
+    });
+    return CSPQ_OK;
+}
+
+}  // namespace cspq

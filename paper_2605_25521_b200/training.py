@@ -1,0 +1,242 @@
+"""Per-subspace codebook training on the B200 -- the drop-in for
+``cspq.training`` (/root/reference/pkg/src/cspq/training.py).
+
+The reference trains subspaces one after another on the CPU (numpy/BLAS
+float64 Lloyd, training.py:109-159, after k-means++ seeding,
+training.py:76-92).  Here all M subspaces of a call are trained together
+on the GPU: one batched k-means++ (``cspq_kmeanspp``) and one batched
+Lloyd run (``cspq_lloyd_train``), each subspace keeping its own stop
+decision, objective trace and iteration count.  Host-side work is limited
+to what the reference also does with numpy's generator: the per-subspace
+PCG64 streams (training.py:162-163), the row sample (training.py:166-172),
+the seeding draws, and input validation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from ._device import device, ptr, stream_ptr, to_device, torch
+from .core import Codebook, DataError, TrainingError
+
+__all__ = [
+    "TrainConfig", "KMeansResult", "lloyd_iterate", "lloyd_iterate_batched", "run_lloyd",
+    "kmeanspp_init_batched", "train_codebook", "train_codebook_report", "train_all_codebooks",
+    "train_all_codebooks_report",
+]
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """training.py:21-43: k, max_iters, tol (relative improvement stop), seed,
+    sample_cap (None -> 256*k points per subspace; <= 0 -> all points)."""
+
+    k: int = 256
+    max_iters: int = 25
+    tol: float = 1e-4
+    seed: int = 0
+    sample_cap: int | None = None
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise TrainingError(f"k must be >= 1, got {self.k}")
+        if self.max_iters < 1:
+            raise TrainingError(f"max_iters must be >= 1, got {self.max_iters}")
+        if self.tol < 0:
+            raise TrainingError(f"tol must be >= 0, got {self.tol}")
+
+    def resolved_cap(self) -> int | None:
+        if self.sample_cap is None:
+            return 256 * self.k
+        return None if self.sample_cap <= 0 else self.sample_cap
+
+
+@dataclass
+class KMeansResult:
+    """training.py:46-54: float32 centroids, objective trace (one value per
+    iteration plus the final-pass objective), final assignments."""
+
+    centroids: np.ndarray
+    objectives: list[float] = field(default_factory=list)
+    assignments: np.ndarray | None = None
+    n_train: int = 0
+    iterations: int = 0
+
+
+def _stack_points(points_list):
+    """[(n, sub)] -> (m, n, sub) contiguous, float32 when every value is
+    exactly representable (the usual float64(float32) training input),
+    else float64."""
+    P = np.ascontiguousarray(np.stack([np.asarray(p, dtype=np.float64) for p in points_list]))
+    P32 = P.astype(np.float32)
+    if np.array_equal(P32.astype(np.float64), P, equal_nan=True):
+        return P32, 0
+    return P, 1
+
+
+def lloyd_iterate_batched(points, init, cfg: TrainConfig, dev=None) -> list[KMeansResult]:
+    """Lloyd from given float64 initial centroids for m subspaces at once.
+
+    points: (m, n, sub) array (float32 or float64) or a list of (n, sub);
+    init: (m, k, sub) float64.  Each subspace follows training.py:109-159
+    exactly, including its own early stop."""
+    N.require_cuda()
+    t = torch()
+    if isinstance(points, t.Tensor):  # device-resident (m, n, sub) float32/float64
+        P = points.contiguous()
+        pf64 = 1 if P.dtype == t.float64 else 0
+        if P.dtype not in (t.float32, t.float64):
+            P, pf64 = P.float(), 0
+    elif isinstance(points, (list, tuple)) or np.asarray(points).dtype != np.float32:
+        P, pf64 = _stack_points(points if isinstance(points, (list, tuple)) else list(np.asarray(points)))
+    else:
+        P, pf64 = np.ascontiguousarray(points, dtype=np.float32), 0
+    C = np.array(init, dtype=np.float64, copy=True, order="C")
+    m, n, sub = P.shape
+    k = C.shape[1]
+    if C.shape != (m, k, sub):
+        raise TrainingError(f"initial centroids {C.shape} do not match points {P.shape}")
+    dev = device() if dev is None else dev
+    with t.cuda.device(dev):
+        Pd = P if isinstance(P, t.Tensor) and P.device == dev else to_device(P, dev)
+        Cd = to_device(C, dev)
+        ws = t.zeros(N.load().cspq_lloyd_workspace_bytes(n, m, sub, k), dtype=t.uint8, device=dev)
+        C32 = t.empty((m, k, sub), dtype=t.float32, device=dev)
+        asg = t.empty((m, n), dtype=t.int32, device=dev)
+        objs = t.zeros((m, cfg.max_iters + 1), dtype=t.float64, device=dev)
+        iters = t.zeros((m,), dtype=t.int32, device=dev)
+        N.call("cspq_lloyd_train", ptr(Pd), pf64, n, m, sub, k, ptr(Cd), cfg.max_iters, float(cfg.tol),
+               ptr(C32), ptr(asg), ptr(objs), ptr(iters), ptr(ws), stream_ptr(dev))
+        C32h, asgh, objh, ith = (x.cpu().numpy() for x in (C32, asg, objs, iters))
+    out = []
+    for j in range(m):
+        it = int(ith[j])
+        out.append(KMeansResult(centroids=np.ascontiguousarray(C32h[j]),
+                                objectives=[float(v) for v in objh[j, :it + 1]],
+                                assignments=asgh[j].astype(np.int64), n_train=n, iterations=it))
+    return out
+
+
+def lloyd_iterate(pts64: np.ndarray, centroids: np.ndarray, cfg: TrainConfig) -> KMeansResult:
+    """training.py:109-159 for one subspace (float64 points, float64 init)."""
+    P = np.asarray(pts64, dtype=np.float64)
+    return lloyd_iterate_batched([P], np.asarray(centroids, dtype=np.float64)[None], cfg)[0]
+
+
+def kmeanspp_init_batched(points_list, k: int, rngs, dev=None) -> np.ndarray:
+    """training.py:76-92 for m subspaces: the host draws exactly what the
+    reference draws from each generator (rng.integers(n), then one
+    rng.random() per rng.choice), the GPU does the D^2 arithmetic."""
+    N.require_cuda()
+    t = torch()
+    P, pf64 = _stack_points(points_list)
+    m, n, sub = P.shape
+    first = np.array([int(r.integers(n)) for r in rngs], dtype=np.int64)
+    u = np.stack([r.random(k - 1) if k > 1 else np.zeros(0) for r in rngs]).astype(np.float64)
+    u = np.ascontiguousarray(u.reshape(m, max(k - 1, 0)))
+    dev = device() if dev is None else dev
+    with t.cuda.device(dev):
+        Pd = to_device(P, dev)
+        fd = to_device(first, dev)
+        ud = to_device(u if u.size else np.zeros((m, 1)), dev)
+        C = t.zeros((m, k, sub), dtype=t.float64, device=dev)
+        status = t.zeros((m,), dtype=t.int32, device=dev)
+        ws = t.zeros(N.load().cspq_lloyd_workspace_bytes(n, m, sub, k), dtype=t.uint8, device=dev)
+        N.call("cspq_kmeanspp", ptr(Pd), pf64, n, m, sub, k, ptr(fd), ptr(ud), ptr(C), ptr(status), ptr(ws),
+               stream_ptr(dev))
+        Ch, st = C.cpu().numpy(), status.cpu().numpy()
+    if (st != 0).any():
+        j = int(np.flatnonzero(st)[0])
+        raise TrainingError(f"subspace {j}: k-means++ found zero remaining D^2 mass "
+                            "(degenerate data; the reference would switch to uniform draws)")
+    return Ch
+
+
+def _validate_points(pts64: np.ndarray, k: int):
+    n = pts64.shape[0]
+    if n < k:
+        raise TrainingError(f"need at least k={k} training points, got {n}")
+    if k > 1 and np.unique(pts64, axis=0).shape[0] < k:
+        raise TrainingError(f"degenerate data: fewer than k={k} distinct training points")
+
+
+def run_lloyd(points: np.ndarray, cfg: TrainConfig, rng: np.random.Generator) -> KMeansResult:
+    """k-means++ seeding plus Lloyd for one subspace (training.py:95-106)."""
+    pts64 = np.asarray(points, dtype=np.float64)
+    _validate_points(pts64, cfg.k)
+    init = kmeanspp_init_batched([pts64], cfg.k, [rng])
+    return lloyd_iterate_batched([pts64], init, cfg)[0]
+
+
+def _subspace_rngs(seed: int, m: int) -> list[np.random.Generator]:
+    """training.py:162-163: one PCG64 stream per subspace."""
+    return [np.random.Generator(np.random.PCG64(s)) for s in np.random.SeedSequence(seed).spawn(m)]
+
+
+def _sample(points: np.ndarray, cap: int | None, rng: np.random.Generator) -> np.ndarray:
+    """training.py:166-172: sorted sample without replacement when above the cap."""
+    if cap is None or points.shape[0] <= cap:
+        return points
+    idx = rng.choice(points.shape[0], size=cap, replace=False)
+    idx.sort()
+    return points[idx]
+
+
+def _train_many(subspace_points, cfg: TrainConfig, rngs, labels):
+    """Sample, validate, seed and train a list of subspaces together."""
+    sampled = []
+    for pts, rng, j in zip(subspace_points, rngs, labels):
+        try:
+            s = _sample(pts, cfg.resolved_cap(), rng)
+            s64 = np.asarray(s, dtype=np.float64)
+            _validate_points(s64, cfg.k)
+        except (TrainingError, DataError) as exc:
+            raise type(exc)(f"subspace {j}: {exc}") from None
+        sampled.append(s64)
+    init = kmeanspp_init_batched(sampled, cfg.k, rngs)
+    return lloyd_iterate_batched(sampled, init, cfg)
+
+
+def train_codebook(subvectors: np.ndarray, cfg: TrainConfig, subspace_index: int = 0) -> Codebook:
+    return train_codebook_report(subvectors, cfg, subspace_index)[0]
+
+
+def train_codebook_report(subvectors: np.ndarray, cfg: TrainConfig,
+                          subspace_index: int = 0) -> tuple[Codebook, KMeansResult]:
+    """training.py:180-194: the subspace's own generator is the
+    (subspace_index)-th child of SeedSequence(cfg.seed)."""
+    pts = np.asarray(subvectors, dtype=np.float32)
+    if pts.ndim != 2:
+        raise TrainingError(f"training points must be 2-D, got shape {pts.shape}")
+    if not np.isfinite(pts).all():
+        raise DataError(f"non-finite training data in subspace {subspace_index}")
+    rng = _subspace_rngs(cfg.seed, subspace_index + 1)[subspace_index]
+    s = _sample(pts, cfg.resolved_cap(), rng)
+    s64 = np.asarray(s, dtype=np.float64)
+    _validate_points(s64, cfg.k)
+    init = kmeanspp_init_batched([s64], cfg.k, [rng])
+    res = lloyd_iterate_batched([s64], init, cfg)[0]
+    return Codebook.from_rowmajor(subspace_index, res.centroids), res
+
+
+def train_all_codebooks(dataset, params, cfg: TrainConfig) -> list[Codebook]:
+    return train_all_codebooks_report(dataset, params, cfg)[0]
+
+
+def train_all_codebooks_report(dataset, params, cfg: TrainConfig):
+    """training.py:203-224: one codebook per subspace from its own sample.
+    Accepts a VectorDataset or a raw (n, d) array (the reference's
+    ``hasattr(dataset, "data")`` probe mistakes an ndarray's buffer for a
+    dataset -- SURVEY §0.6; here raw arrays simply work)."""
+    data = dataset.data if isinstance(getattr(dataset, "data", None), np.ndarray) else np.asarray(dataset, dtype=np.float32)
+    if data.shape[1] != params.d:
+        raise TrainingError(f"dataset dimensionality {data.shape[1]} does not match d={params.d}")
+    rngs = _subspace_rngs(cfg.seed, params.m)
+    sub = params.sub_dim
+    pts = [np.ascontiguousarray(data[:, j * sub:(j + 1) * sub]) for j in range(params.m)]
+    reports = _train_many(pts, cfg, rngs, range(params.m))
+    return [Codebook.from_rowmajor(j, r.centroids) for j, r in enumerate(reports)], reports

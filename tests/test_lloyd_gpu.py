@@ -1,0 +1,188 @@
+"""Parity of the GPU Lloyd / k-means++ path with the reference's golden runs
+and the oracle, mirroring pkg/tests/test_training.py."""
+
+import numpy as np
+import pytest
+
+from conftest import cases, golden, group
+
+pytestmark = pytest.mark.gpu
+
+LLOYD = golden("lloyd_golden.npz")
+TRAIN = golden("train_golden.npz")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2605_25521_b200 as P
+    return P
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return (np.linalg.norm(a - b, axis=-1) / np.maximum(np.linalg.norm(b, axis=-1), 1e-30)).max()
+
+
+@pytest.mark.parametrize("case", cases(LLOYD))
+def test_lloyd_vs_reference_golden(P, case):
+    g = group(LLOYD, case)
+    cfg = P.TrainConfig(k=g["init"].shape[0], max_iters=int(g["max_iters"]), tol=float(g["tol"]))
+    r = P.lloyd_iterate(g["pts"].astype(np.float64), g["init"], cfg)
+    assert r.iterations == int(g["iterations"])
+    assert np.array_equal(r.assignments, g["assignments"])
+    assert rel_err(r.centroids, g["centroids"]) <= 1e-5
+    np.testing.assert_allclose(r.objectives, g["objectives"], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("case", cases(LLOYD))
+def test_lloyd_vs_oracle_bitwise(P, oracle, case):
+    g = group(LLOYD, case)
+    pts = g["pts"].astype(np.float64)
+    o = oracle.lloyd(pts, g["init"], int(g["max_iters"]), float(g["tol"]))
+    r = P.lloyd_iterate(pts, g["init"], P.TrainConfig(k=g["init"].shape[0], max_iters=int(g["max_iters"]),
+                                                      tol=float(g["tol"])))
+    assert r.iterations == o["iterations"]
+    assert r.centroids.tobytes() == o["centroids"].tobytes()
+    assert np.array_equal(r.assignments, o["assignments"])
+    assert r.objectives == o["objectives"]
+
+
+def test_batched_subspaces_stop_independently(P, oracle):
+    rng = np.random.default_rng(5)
+    m, n, sub, k = 6, 3000, 4, 32
+    pts = []
+    for j in range(m):
+        cen = rng.uniform(-5, 5, (k, sub)) * (j + 1)
+        pts.append((cen[rng.integers(0, k, n)] + rng.normal(0, 0.3 + 0.2 * j, (n, sub))).astype(np.float32))
+    init = np.stack([p[np.sort(rng.choice(n, k, replace=False))] for p in pts]).astype(np.float64)
+    cfg = P.TrainConfig(k=k, max_iters=30, tol=1e-3)
+    res = P.lloyd_iterate_batched(np.stack(pts), init, cfg)
+    iters = set()
+    for j in range(m):
+        o = oracle.lloyd(pts[j].astype(np.float64), init[j], 30, 1e-3)
+        assert res[j].iterations == o["iterations"]
+        assert res[j].centroids.tobytes() == o["centroids"].tobytes()
+        assert res[j].objectives == o["objectives"]
+        iters.add(res[j].iterations)
+    assert len(iters) > 1  # subspaces really stopped at different iterations
+
+
+def test_kmeanspp_default_path_vs_reference(P):
+    """train_all_codebooks_report with the reference's defaults (per-subspace
+    sampling + k-means++ + tol stop) against the reference's own run."""
+    X = TRAIN["kmpp/X"]
+    params = P.PQParams(d=32, m=4, k=64)
+    cfg = P.TrainConfig(k=64, seed=11, sample_cap=3000, max_iters=12)
+    cbs, reps = P.train_all_codebooks_report(P.VectorDataset(data=np.array(X)), params, cfg)
+    ref = TRAIN["kmpp/centroids"]
+    for j in range(4):
+        assert reps[j].iterations == int(TRAIN[f"kmpp/iterations_{j}"])
+        assert np.array_equal(reps[j].assignments, TRAIN[f"kmpp/assignments_{j}"])
+        assert rel_err(cbs[j].centroids_rowmajor, ref[j]) <= 1e-5
+        np.testing.assert_allclose(reps[j].objectives, TRAIN[f"kmpp/objectives_{j}"], rtol=1e-12)
+        assert cbs[j].biases.tobytes() == P.compute_biases(cbs[j].centroids_rowmajor).tobytes()
+
+
+def test_kmeanspp_seeding_matches_reference(P):
+    from paper_2605_25521_b200.training import _sample, _subspace_rngs, kmeanspp_init_batched
+    X = TRAIN["kmpp/X"]
+    rngs = _subspace_rngs(11, 4)
+    pts = np.ascontiguousarray(X[:, 8:16])
+    sampled = _sample(pts, 3000, rngs[1])
+    init = kmeanspp_init_batched([sampled.astype(np.float64)], 64, [rngs[1]])[0]
+    assert init.tobytes() == TRAIN["kmpp/seed_init_sub1"].tobytes()
+
+
+# ---- pkg/tests/test_training.py on the GPU ----
+
+def test_separable_pair(P):
+    cb, rep = P.train_codebook_report(np.array([[0.0], [10.0]], np.float32), P.TrainConfig(k=2, seed=0))
+    assert sorted(cb.centroids_rowmajor[:, 0].tolist()) == [0.0, 10.0]
+    assert rep.objectives[-1] == 0.0
+
+
+def test_single_cluster_mean(P):
+    cb, rep = P.train_codebook_report(np.array([[1.0], [3.0]], np.float32), P.TrainConfig(k=1, seed=0))
+    assert cb.centroids_rowmajor[0, 0] == pytest.approx(2.0)
+    assert rep.objectives[-1] == pytest.approx(2.0)
+
+
+def test_training_errors(P):
+    with pytest.raises(P.TrainingError):
+        P.train_codebook(np.zeros((2, 3), np.float32), P.TrainConfig(k=5))
+    with pytest.raises(P.TrainingError, match="degenerate"):
+        P.train_codebook(np.full((50, 2), 7.0, np.float32), P.TrainConfig(k=2))
+    data = np.array([[0.0, 5.0], [10.0, 5.0]], np.float32)
+    with pytest.raises(P.TrainingError, match="subspace 1"):
+        P.train_all_codebooks(data, P.PQParams(d=2, m=2, k=2), P.TrainConfig(k=2, seed=0))
+
+
+def test_k1_means_raw_array(P):
+    data = np.array([[0.0, 5.0], [10.0, 5.0]], np.float32)
+    cbs = P.train_all_codebooks(data, P.PQParams(d=2, m=2, k=1), P.TrainConfig(k=1, seed=0))
+    assert cbs[0].centroids_rowmajor[0, 0] == pytest.approx(5.0)
+    assert cbs[1].centroids_rowmajor[0, 0] == pytest.approx(5.0)
+
+
+def _synth(n, d, clusters, seed, noise=0.05):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    means = rng.uniform(-1.0, 1.0, size=(clusters, d)).astype(np.float32)
+    labels = rng.integers(0, clusters, size=n)
+    return (means[labels] + rng.normal(0.0, noise, size=(n, d)).astype(np.float32)).astype(np.float32)
+
+
+def test_monotone_deterministic_consistent(P):
+    X = _synth(4000, 16, 8, 0)
+    params, cfg = P.PQParams(d=16, m=2, k=32), P.TrainConfig(k=32, seed=0)
+    a, reps = P.train_all_codebooks_report(X, params, cfg)
+    for rep in reps:
+        for x, y in zip(rep.objectives, rep.objectives[1:]):
+            assert y <= x * (1 + 1e-4)
+    b = P.train_all_codebooks(X, params, cfg)
+    for x, y in zip(a, b):
+        assert x.centroids_rowmajor.tobytes() == y.centroids_rowmajor.tobytes()
+    pts = X[:1500, :8]
+    cb, rep = P.train_codebook_report(pts, P.TrainConfig(k=16, seed=5))
+    for i in range(0, 1500, 97):
+        assert P.encode_ref(pts[i], cb) == rep.assignments[i]
+
+
+def test_sample_cap_and_repair(P):
+    pts = _synth(5000, 4, 4, 6)
+    _, rep = P.train_codebook_report(pts, P.TrainConfig(k=4, seed=6, sample_cap=500))
+    assert rep.n_train == 500
+    _, rep = P.train_codebook_report(pts, P.TrainConfig(k=4, seed=6, sample_cap=0))
+    assert rep.n_train == 5000
+    res = P.lloyd_iterate(np.array([[0.0], [0.1], [0.2], [10.0], [10.1], [50.0]]),
+                          np.array([[0.0], [0.0], [10.0]]), P.TrainConfig(k=3, max_iters=10, seed=0))
+    assert np.all(np.bincount(res.assignments, minlength=3) >= 1)
+    assert any(abs(c - 50.0) < 1e-6 for c in res.centroids[:, 0])
+
+
+def test_subspace_independence(P):
+    X = _synth(2000, 8, 4, 3)
+    cfg = P.TrainConfig(k=8, seed=77)
+    cbs = P.train_all_codebooks(X, P.PQParams(d=8, m=2, k=8), cfg)
+    solo = P.train_codebook(X[:, 4:8], cfg, subspace_index=1)
+    assert cbs[1].centroids_rowmajor.tobytes() == solo.centroids_rowmajor.tobytes()
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_config_training_vs_oracle(P, oracle, name):
+    """Config-shaped training (sample-point init, tol 0) at reduced sample
+    size: GPU == oracle bit for bit for a few subspaces."""
+    import torch
+    from paper_2605_25521_b200 import configs as C
+    cfg = C.CONFIGS[name].scaled(n=200_000, n_train=20_000)
+    dev = torch.device("cuda", 0)
+    S = C.training_sample(cfg, dev)
+    Ssm = C.subspace_major(S, cfg.m)[:4]
+    init = C.lloyd_init(cfg, Ssm)
+    res = P.lloyd_iterate_batched(Ssm, init, P.TrainConfig(k=cfg.k, max_iters=cfg.iters, tol=0.0))
+    Sh = Ssm.cpu().numpy()
+    for j in range(4):
+        o = oracle.lloyd(Sh[j].astype(np.float64), init[j], cfg.iters, 0.0)
+        assert res[j].iterations == o["iterations"]
+        assert res[j].centroids.tobytes() == o["centroids"].tobytes(), (name, j)
+        assert res[j].objectives == o["objectives"]
