@@ -1,0 +1,296 @@
+#!/usr/bin/env python
+"""bench.py -- PQ-encoded vectors/s on B200 (BASELINE.json metric).
+
+Workload (default): BASELINE config 3 -- N = 10,000,000 unit-normalised
+float32 rows per GPU, D = 768, M = 96 subspaces (d_sub = 8), K = 256,
+codebooks from 10 Lloyd iterations (GPU, fp64) on a 200,000-row seeded
+sample, trained on rank 0 and broadcast over NCCL.  A "step" is one encode
+pass of the whole shard (one fused kernel launch).  Weak scaling: every rank
+encodes its own 10M-row shard of one seeded dataset (rows r*N .. (r+1)*N).
+
+Launch: python bench.py [--gpus N --steps K --warmup W]
+        torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+        python bench.py --impl reference ...   (the CPU oracle, host cores)
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PQ-encoded vectors/sec"
+FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.45: SMs x FP32 lanes x FMA x max clock
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--rows", type=int, default=0, help="rows per rank (0 = the config's N)")
+    p.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    p.add_argument("--mode", default="auto", choices=["auto", "exact", "guarded"])
+    p.add_argument("--e2e-rows", type=int, default=2_000_000)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_desc(cfg, rows_per_rank, ws, scaling):
+    return (f"{cfg.name}: {'u8' if cfg.dtype == 'u8' else 'f32'} rows D={cfg.d}, M={cfg.m} (d_sub={cfg.sub}), "
+            f"K={cfg.k}, {rows_per_rank:,} rows/GPU ({scaling} scaling), codebooks: "
+            + (f"{cfg.iters} Lloyd iters on a {cfg.n_train:,}-row sample" if cfg.codebook == "lloyd"
+               else "256 distinct data subvectors per subspace"))
+
+
+def oracle_codebooks(cfg, dev):
+    """Codebooks for the reference arm: the config's Lloyd initial points
+    (no GPU compute -- only the seeded data generator)."""
+    import numpy as np
+    from paper_2605_25521_b200 import configs as C
+    S = C.training_sample(cfg, dev)
+    rm = np.ascontiguousarray(C.lloyd_init(cfg, C.subspace_major(S, cfg.m)).astype(np.float32))
+    from oracle.oracle import compute_biases
+    return rm, compute_biases(rm)
+
+
+def cpu_oracle_rate(cfg, dev, rm, bs, seconds, rows_hint=50_000):
+    """Time the CPU oracle (strict-fp32 restatement of the reference's
+    encoder, all host threads) on bounded samples of the workload's rows."""
+    import numpy as np
+    from oracle import oracle as O
+    from paper_2605_25521_b200 import configs as C
+    cores = os.cpu_count() or 1
+    warm = C.generate(cfg, 0, min(rows_hint, 20_000), dev).cpu().numpy()
+    O.encode(warm, rm, bs, O.VARIANT_REFORM, threads=cores)
+    t0 = time.perf_counter()
+    O.encode(warm, rm, bs, O.VARIANT_REFORM, threads=cores)
+    per_row = (time.perf_counter() - t0) / warm.shape[0]
+    rows = int(max(10_000, min(cfg.n, seconds / max(per_row, 1e-9))))
+    X = C.generate(cfg, 0, rows, dev).cpu().numpy()
+    t0 = time.perf_counter()
+    O.encode(X, rm, bs, O.VARIANT_REFORM, threads=cores)
+    dt = time.perf_counter() - t0
+    return rows / dt, rows, dt, cores
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the CPU oracle of the reference's encoder on the
+    host cores, same config/metric; rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+    from paper_2605_25521_b200 import configs as C
+    from oracle import oracle as O
+    cfg = C.CONFIGS[args.config]
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    rm, bs = oracle_codebooks(cfg, dev)
+    cores = os.cpu_count() or 1
+    rate, rows, _, _ = cpu_oracle_rate(cfg, dev, rm, bs, 3.0)
+    X = C.generate(cfg, 0, rows, dev).cpu().numpy()
+    for _ in range(args.warmup):
+        O.encode(X, rm, bs, O.VARIANT_REFORM, threads=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.encode(X, rm, bs, O.VARIANT_REFORM, threads=cores)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = rows / (ms / 1e3)
+    sample = f"{rows:,} rows of {cfg.name} per step (oracle/pq_oracle.c, strict fp32, {cores} threads)"
+    line = {
+        "metric": METRIC, "value": value, "unit": "vectors/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": workload_desc(cfg, rows, 1, args.scaling), "rows_per_step": rows},
+        "cpu_baseline": {"value": value, "unit": "vectors/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "vectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_25521_b200 as P
+    from paper_2605_25521_b200 import _native as N
+    from paper_2605_25521_b200 import configs as C
+    from paper_2605_25521_b200.telemetry import ClockSampler
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = C.CONFIGS[args.config]
+    rows = args.rows or cfg.n
+    if args.scaling == "strong":
+        rows = rows // ws
+    begin = rank * rows
+
+    # ---- data (device-resident, seeded, chunk-deterministic) ----
+    X = C.generate(cfg, begin, begin + rows, dev)
+
+    # ---- codebooks: GPU Lloyd on rank 0, NCCL broadcast ----
+    rm = torch.empty((cfg.m, cfg.k, cfg.sub), dtype=torch.float32, device=dev)
+    train_s = None
+    if rank == 0:
+        if cfg.codebook == "sampled":
+            Xh = C.generate(cfg, 0, cfg.n, dev).cpu().numpy()
+            rm.copy_(torch.from_numpy(C.sampled_codebooks(cfg, Xh)))
+        else:
+            S = C.training_sample(cfg, dev)
+            Ssm = C.subspace_major(S, cfg.m)
+            init = C.lloyd_init(cfg, Ssm)
+            t0 = time.perf_counter()
+            res = P.lloyd_iterate_batched(Ssm, init, P.TrainConfig(k=cfg.k, max_iters=cfg.iters, tol=0.0))
+            train_s = time.perf_counter() - t0
+            rm.copy_(torch.from_numpy(np.stack([r.centroids for r in res])))
+            del S, Ssm
+    if ws > 1:
+        dist.broadcast(rm, src=0)
+    rmh = rm.cpu().numpy()
+    cs = P.CodebookSet.from_codebooks([P.Codebook.from_rowmajor(j, rmh[j]) for j in range(cfg.m)])
+    plan = P.ExecutionPlan(mode=args.mode)
+    out = P.encode_dataset_device(X, cs, plan)
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+
+    # ---- parity spot-check vs the oracle (rank 0, sampled rows) ----
+    parity = None
+    if rank == 0:
+        from oracle import oracle as O
+        rng = np.random.default_rng(123)
+        idx = np.sort(rng.choice(rows, min(rows, 20_000), replace=False))
+        ti = torch.from_numpy(idx).to(dev)
+        want = O.encode(X[ti].cpu().numpy(), cs.rowmajor, cs.biases, O.VARIANT_REFORM)
+        got = out[ti].cpu().numpy()
+        parity = {"rows_checked": int(idx.shape[0]), "code_mismatches": int((got != want).sum())}
+
+    # ---- device-resident timed region ----
+    for _ in range(args.warmup):
+        P.encode_dataset_device(X, cs, plan, out=out)
+    N.call("cspq_encode_stats", None, 1)
+    clocks = ClockSampler(local).start()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for s in range(args.steps):
+        P.encode_dataset_device(X, cs, plan, out=out)
+        ev[s + 1].record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    fl = ctypes.c_uint64(0)
+    N.call("cspq_encode_stats", ctypes.byref(fl), 1)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = rows * ws * args.steps / (total_ms / 1e3)
+
+    # ---- end-to-end through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        ne = min(args.e2e_rows, rows)
+        Xh = P.pinned_empty((ne, cfg.d), np.uint8 if cfg.dtype == "u8" else np.float32)
+        Xh[:] = X[:ne].cpu().numpy()
+        codes_h = P.pinned_empty((ne, cfg.m), np.uint8)
+        eplan = P.ExecutionPlan(mode=args.mode, batch_rows=1 << 18, streams=3)
+        P.encode_dataset_host(Xh, cs, eplan, out=codes_h)  # warm the pipeline
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            P.encode_dataset_host(Xh, cs, eplan, out=codes_h)
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e_val = ne * ws * args.steps / float(el.item())
+        assert np.array_equal(codes_h[:4096], out[:4096].cpu().numpy()), "e2e codes differ from device codes"
+        e2e = {"value": e2e_val, "unit": "vectors/s", "h2d_bytes_per_step": int(ne * cfg.d * cfg.elem_bytes) * ws,
+               "d2h_bytes_per_step": int(ne * cfg.m) * ws, "rows_per_gpu": ne,
+               "path": "encode_dataset_host (pinned numpy -> cspq_encode_host: 3-stream H2D/encode/D2H pipeline)"}
+
+    # ---- roofline of the encode kernel ----
+    flops_launch = rows * cfg.flops_per_vec()
+    achieved = flops_launch / (ms_per_step / 1e3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "encode_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            bpr = tj.get(cfg.name, {}).get("dram_bytes_per_row")
+            traffic = None if bpr is None else int(bpr * rows)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP32_NOMINAL_TFLOPS, "traffic": traffic,
+                "kernel": "encode_k256_kernel (guarded FFMA)" if args.mode != "exact" else "encode_k256_kernel (exact)",
+                "peak_source": "nominal FP32: 148 SMs x 128 lanes x 2 flop x 1.965 GHz (no FP32 entry in MEASURED_PEAKS.json)",
+                "algorithmic_flops_per_row": cfg.flops_per_vec(),
+                "algorithmic_bytes_per_row": cfg.bytes_per_vec(),
+                "hbm_frac": (rows * cfg.bytes_per_vec() / (ms_per_step / 1e3) / 1e9) / 6547.8}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rate, crow, cdt, cores = cpu_oracle_rate(cfg, dev, cs.rowmajor, cs.biases, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "vectors/s", "cores": cores, "kind": "port",
+               "sample": f"{crow:,} rows of {cfg.name} in {cdt:.1f} s (oracle/pq_oracle.c strict-fp32 restatement of "
+                         f"the reference encoder, OpenMP over all host threads)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "vectors/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg, rows, ws, args.scaling), "global_batch": rows * ws,
+                       "rows_per_gpu": rows, "parallelism": f"rows sharded x{ws} (codebooks NCCL-broadcast)",
+                       "mode": args.mode, "codebook_train_s": train_s, "l2": "inputs larger than L2 (30.7 GB/GPU)" if cfg.name == "c3"
+                       else "inputs larger than L2"},
+            "clocks": clk, "e2e": e2e, "gpu_launches": args.steps, "roofline": roofline, "cpu_baseline": cpu,
+            "parity": parity, "flagged_per_subvector": fl.value / max(1, rows * cfg.m * args.steps),
+            "step_ms": step_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -77,6 +77,18 @@ const char *cspq_last_error(void);
 int cspq_encode_prepare(const float *CB, const float *B, int32_t m, int32_t k, int32_t sub,
                         float *guard, void *stream);
 
+/* Tuning knob for benchmarks: thread-block tiling of the fast encode kernel
+ * (0 = 8 rows x 128 threads, 2 CTAs/SM; 1 = 8 x 128, 3 CTAs/SM;
+ * 2 = 4 rows x 256 threads; 3 = 4 rows x 128 threads, 4 CTAs/SM [default]).
+ * Process-global; never changes the codes. */
+int cspq_encode_set_tiling(int32_t tiling);
+
+/* Telemetry of the fast encode kernels (device-global, all streams):
+ * number of (row, subspace) pairs whose best score had a runner-up inside
+ * the guard band and were therefore re-encoded exactly.  Synchronises the
+ * device.  reset != 0 zeroes the counter after reading. */
+int cspq_encode_stats(uint64_t *flagged, int32_t reset);
+
 /* Bias table of the precomputed_bias=False ablation (kernels.py:146-157):
  * B_out[j,l] = 0.5f * fl-chain(sum_t c_t*c_t) in float32, exactly as the
  * reference recomputes it per vector.  (m, k) float32 device buffer. */

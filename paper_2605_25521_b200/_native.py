@@ -33,6 +33,8 @@ _i32, _i64, _vp, _dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.
 _SIGS = {
     "cspq_abi_version": ([], _i32),
     "cspq_last_error": ([], ctypes.c_char_p),
+    "cspq_encode_stats": ([_vp, _i32], _i32),
+    "cspq_encode_set_tiling": ([_i32], _i32),
     "cspq_encode_prepare": ([_vp, _vp, _i32, _i32, _i32, _vp, _vp], _i32),
     "cspq_recompute_biases_f32": ([_vp, _i32, _i32, _i32, _vp, _vp], _i32),
     "cspq_encode": ([_vp, _i32, _i64, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _i32, _vp], _i32),

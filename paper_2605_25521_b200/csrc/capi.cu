@@ -15,6 +15,8 @@ namespace cspq {
 
 // kernels (encode.cu / lloyd.cu)
 int encode_prepare(const float *CB, const float *B, int m, int k, int sub, float *guard, cudaStream_t st);
+int encode_stats(unsigned long long *flagged, int reset);
+int encode_set_tiling(int t);
 int recompute_biases(const float *CB, int m, int k, int sub, float *Bo, cudaStream_t st);
 int encode_device(const void *X, int in_dtype, int64_t n, int d, int64_t xrs, const float *CB, const float *B,
                   const float *guard, int m, int k, int sub, void *codes, int64_t crs, int variant, int mode,
@@ -144,6 +146,15 @@ extern "C" {
 
 int cspq_abi_version(void) { return CSPQ_ABI_VERSION; }
 const char *cspq_last_error(void) { return g_err; }
+
+int cspq_encode_set_tiling(int32_t tiling) { return encode_set_tiling(tiling); }
+
+int cspq_encode_stats(uint64_t *flagged, int32_t reset) {
+    unsigned long long v = 0;
+    int rc = encode_stats(flagged ? &v : nullptr, reset);
+    if (flagged) *flagged = v;
+    return rc;
+}
 
 int cspq_encode_prepare(const float *CB, const float *B, int32_t m, int32_t k, int32_t sub, float *guard,
                         void *stream) {

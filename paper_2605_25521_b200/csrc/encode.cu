@@ -38,7 +38,6 @@ namespace cspq {
 
 namespace {
 
-constexpr int kT = 128;    // threads per CTA
 constexpr int kK = 256;    // centroids (fast path)
 constexpr int kBlk = 8;    // centroids per argmin block
 
@@ -77,8 +76,29 @@ __device__ __forceinline__ void load_cent(const float *p, float (&c)[SUB]) {
     }
 }
 
+// tiling of the fast kernel (cspq_encode_set_tiling; default 3, the fastest
+// on B200 in scripts/sweep_tiling.py): 0 = R8/T128/2 CTAs,
+// 1 = R8/T128/3, 2 = R4/T256/2, 3 = R4/T128/4 -- codes never depend on it
+int g_tiling = 3;
+
+// flagged-subvector counter (telemetry: cspq_encode_stats)
+__device__ unsigned long long g_flagged = 0;
+
 // gamma_n = n u / (1 - n u), u = 2^-24
 __host__ __device__ constexpr double gamma_n(int n) { return n * 5.9604644775390625e-8 / (1.0 - n * 5.9604644775390625e-8); }
+
+// Shared-memory codebook: one record per block of kBlk centroids = the
+// block's centroids (kBlk*SUB floats) followed by its kBlk biases, padded
+// to an odd number of 16-byte chunks so that lanes reading different
+// records (the winner-block re-score) spread over all 8 bank groups.
+template <int SUB>
+struct Rec {
+    static constexpr int kChunks = (kBlk * SUB + kBlk) / 4;                 // 16-byte chunks of payload
+    static constexpr int kStride = (kChunks % 2 == 0) ? kChunks + 1 : kChunks;  // chunks per record
+    static constexpr int kFloats = kStride * 4;
+    static constexpr int kBias = kBlk * SUB;                                 // bias offset in a record
+    static constexpr int kTotal = (kK / kBlk) * kFloats;                     // floats per staged codebook
+};
 
 template <int SUB, typename TIn>
 struct TileCopy {
@@ -102,12 +122,13 @@ struct TileCopy {
 // ---------------------------------------------------------------------------
 // Fast path: k = 256, sub in {4, 8}, f32 or u8 rows.
 // ---------------------------------------------------------------------------
-template <int SUB, int R, typename TIn, bool EXACT>
-__global__ void __launch_bounds__(kT, 2)
+template <int SUB, int R, int kT, int MINB, typename TIn, bool EXACT>
+__global__ void __launch_bounds__(kT, MINB)
 encode_k256_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs,
                    const float *__restrict__ CB, const float *__restrict__ B,
                    const float *__restrict__ guard, uint8_t *__restrict__ codes, int64_t cs) {
-    constexpr int CBF = kK * SUB + kK;  // floats per staged codebook (centroids + biases)
+    using RC = Rec<SUB>;
+    constexpr int CBF = RC::kTotal;     // floats per staged codebook (records)
     constexpr int XE = R * kT * SUB;    // elements per staged x tile
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *cbuf = reinterpret_cast<float *>(smem_raw);
@@ -121,8 +142,13 @@ encode_k256_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs,
         const float *gc = CB + (int64_t)j * kK * SUB;
         const float *gb = B + (int64_t)j * kK;
         float *sc = cbuf + buf * CBF;
-        for (int q = tid; q < kK * SUB / 4; q += kT) cp_async16(sc + 4 * q, gc + 4 * q);
-        for (int q = tid; q < kK / 4; q += kT) cp_async16(sc + kK * SUB + 4 * q, gb + 4 * q);
+        constexpr int CPB = kBlk * SUB / 4;  // centroid chunks per record
+        for (int q = tid; q < (kK / kBlk) * (CPB + kBlk / 4); q += kT) {
+            const int rec = q / (CPB + kBlk / 4), w = q % (CPB + kBlk / 4);
+            float *dst = sc + rec * RC::kFloats + 4 * w;
+            const float *src = w < CPB ? gc + (rec * kBlk * SUB + 4 * w) : gb + (rec * kBlk + 4 * (w - CPB));
+            cp_async16(dst, src);
+        }
         TIn *sx = xbuf + buf * XE;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -142,7 +168,6 @@ encode_k256_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs,
         __syncthreads();
 
         const float *sc = cbuf + (j & 1) * CBF;
-        const float *sb = sc + kK * SUB;
         const TIn *sx = xbuf + (j & 1) * XE;
 
         // this thread's R subvectors (negated for the FFMA chain)
@@ -168,10 +193,10 @@ encode_k256_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs,
 
 #pragma unroll 1
         for (int blk = 0; blk < kK / kBlk; ++blk) {
-            const float *cblk = sc + blk * kBlk * SUB;
+            const float *cblk = sc + blk * RC::kFloats;
             float bb[kBlk];
             {
-                const float4 *bp = reinterpret_cast<const float4 *>(sb + blk * kBlk);
+                const float4 *bp = reinterpret_cast<const float4 *>(cblk + RC::kBias);
 #pragma unroll
                 for (int q = 0; q < kBlk / 4; ++q) {
                     float4 v = bp[q];
@@ -224,18 +249,26 @@ encode_k256_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs,
                 thr = m1[r] + (kG * (gbmax + nrm * gcmax) + 1e-36f);
             }
             if (m1[r] < pos_inf_f()) {
-                const int l0 = wb[r] * kBlk;
+                const float *rec = sc + wb[r] * RC::kFloats;
+                float rb[kBlk];
+                {
+                    const float4 *bp = reinterpret_cast<const float4 *>(rec + RC::kBias);
+#pragma unroll
+                    for (int q = 0; q < kBlk / 4; ++q) {
+                        float4 v = bp[q];
+                        rb[4 * q] = v.x; rb[4 * q + 1] = v.y; rb[4 * q + 2] = v.z; rb[4 * q + 3] = v.w;
+                    }
+                }
                 int first = -1, others = 0;
 #pragma unroll
                 for (int cc = 0; cc < kBlk; ++cc) {
                     float c[SUB];
-                    load_cent<SUB>(sc + (l0 + cc) * SUB, c);
-                    const float s = EXACT ? score_exact<SUB>(x[r], c, sb[l0 + cc])
-                                          : score_ffma<SUB>(x[r], c, sb[l0 + cc]);
+                    load_cent<SUB>(rec + cc * SUB, c);
+                    const float s = EXACT ? score_exact<SUB>(x[r], c, rb[cc]) : score_ffma<SUB>(x[r], c, rb[cc]);
                     if (first < 0 && s == m1[r]) first = cc;
                     else if (!EXACT && s <= thr) ++others;
                 }
-                code[r] = l0 + (first < 0 ? 0 : first);
+                code[r] = wb[r] * kBlk + (first < 0 ? 0 : first);
                 if constexpr (!EXACT) flag[r] = (others > 0) || (m2[r] <= thr) || !(thr < pos_inf_f()) || first < 0;
             } else {
                 if constexpr (!EXACT) flag[r] = true;  // all approximate scores NaN/inf: decide exactly
@@ -247,6 +280,7 @@ encode_k256_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs,
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 unsigned mask = __ballot_sync(0xffffffffu, flag[r]);
+                if (lane == 0 && mask) atomicAdd(&g_flagged, (unsigned long long)__popc(mask));
                 while (mask) {
                     const int src = __ffs(mask) - 1;
                     mask &= mask - 1;
@@ -257,8 +291,9 @@ encode_k256_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs,
                     int bl = kK;
                     for (int l = lane; l < kK; l += 32) {
                         float c[SUB];
-                        load_cent<SUB>(sc + l * SUB, c);
-                        const float s = score_exact<SUB>(xv, c, sb[l]);
+                        const float *rec = sc + (l / kBlk) * RC::kFloats;
+                        load_cent<SUB>(rec + (l % kBlk) * SUB, c);
+                        const float s = score_exact<SUB>(xv, c, rec[RC::kBias + l % kBlk]);
                         if (s < best) { best = s; bl = l; }
                     }
 #pragma unroll
@@ -400,11 +435,11 @@ __global__ void nobias_kernel(const float *__restrict__ CB, int m, int k, int su
     Bo[i] = __fmul_rn(0.5f, acc);
 }
 
-template <int SUB, int R, typename TIn, bool EXACT>
+template <int SUB, int R, int kT, int MINB, typename TIn, bool EXACT>
 int launch_fast(const TIn *X, int64_t n, int m, int64_t xs, const float *CB, const float *B,
                 const float *guard, uint8_t *codes, int64_t cs, cudaStream_t st) {
-    constexpr size_t smem = 2 * (size_t)(kK * SUB + kK) * sizeof(float) + 2 * (size_t)R * kT * SUB * sizeof(TIn);
-    auto kern = encode_k256_kernel<SUB, R, TIn, EXACT>;
+    constexpr size_t smem = 2 * (size_t)Rec<SUB>::kTotal * sizeof(float) + 2 * (size_t)R * kT * SUB * sizeof(TIn);
+    auto kern = encode_k256_kernel<SUB, R, kT, MINB, TIn, EXACT>;
     static bool attr_set = false;  // benign race: idempotent attribute
     if (!attr_set) {
         CSPQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -453,13 +488,26 @@ int dispatch(const TIn *X, int64_t n, int d, int64_t xrs, const float *CB, const
     if (fast) {
         const bool exact = mode == CSPQ_MODE_EXACT;
         uint8_t *c8 = reinterpret_cast<uint8_t *>(codes);
+        const int tiling = g_tiling;
+#define CSPQ_FAST(SUBV, RV, TV, MB)                                                                     \
+    return exact ? launch_fast<SUBV, RV, TV, MB, TIn, true>(X, n, m, xrs, CB, B, guard, c8, crs, st)   \
+                 : launch_fast<SUBV, RV, TV, MB, TIn, false>(X, n, m, xrs, CB, B, guard, c8, crs, st)
         if (sub == 8) {
-            return exact ? launch_fast<8, 8, TIn, true>(X, n, m, xrs, CB, B, guard, c8, crs, st)
-                         : launch_fast<8, 8, TIn, false>(X, n, m, xrs, CB, B, guard, c8, crs, st);
+            switch (tiling) {
+                case 1: CSPQ_FAST(8, 8, 128, 3);
+                case 2: CSPQ_FAST(8, 4, 256, 2);
+                case 3: CSPQ_FAST(8, 4, 128, 4);
+                default: CSPQ_FAST(8, 8, 128, 2);
+            }
         } else {
-            return exact ? launch_fast<4, 8, TIn, true>(X, n, m, xrs, CB, B, guard, c8, crs, st)
-                         : launch_fast<4, 8, TIn, false>(X, n, m, xrs, CB, B, guard, c8, crs, st);
+            switch (tiling) {
+                case 1: CSPQ_FAST(4, 8, 128, 3);
+                case 2: CSPQ_FAST(4, 4, 256, 2);
+                case 3: CSPQ_FAST(4, 4, 128, 4);
+                default: CSPQ_FAST(4, 8, 128, 2);
+            }
         }
+#undef CSPQ_FAST
     }
     (void)d;
     if (reform)
@@ -468,6 +516,21 @@ int dispatch(const TIn *X, int64_t n, int d, int64_t xrs, const float *CB, const
 }
 
 }  // namespace
+
+int encode_set_tiling(int t) {
+    CSPQ_REQUIRE(t >= 0 && t <= 3, CSPQ_E_CONFIG, "tiling must be in [0, 3], got %d", t);
+    g_tiling = t;
+    return CSPQ_OK;
+}
+
+int encode_stats(unsigned long long *flagged, int reset) {
+    if (flagged) CSPQ_CUDA_TRY(cudaMemcpyFromSymbol(flagged, g_flagged, sizeof(unsigned long long)));
+    if (reset) {
+        const unsigned long long z = 0;
+        CSPQ_CUDA_TRY(cudaMemcpyToSymbol(g_flagged, &z, sizeof(z)));
+    }
+    return CSPQ_OK;
+}
 
 int encode_prepare(const float *CB, const float *B, int m, int k, int sub, float *guard, cudaStream_t st) {
     guard_kernel<<<m, 256, 0, st>>>(CB, B, k, sub, guard);
