@@ -113,6 +113,24 @@ int cspq_encode_with_scores(const void *X, int32_t in_dtype, int64_t n, int32_t 
                             const float *CB, const float *B, int32_t m, int32_t k, int32_t sub,
                             int32_t *codes, float *best, int32_t variant, void *stream);
 
+/* Tensor-core encode (tcgen05.mma kind::tf32, sm_100a): the same codes as
+ * cspq_encode -- the oracle's, bit for bit -- computed as a 3xTF32 GEMM with
+ * the bias folded in, an exact argmin/runner-up epilogue on the TMEM
+ * accumulators and an exact fix-up of every subvector whose runner-up lies
+ * within the tensor-core error band.  Needs k == 256, sub in {4, 8},
+ * REFORMULATED/BLOCKED semantics and 16-byte aligned float32 rows (or uint8
+ * rows).  `img` is the prepared codebook image (cspq_encode_tc_prepare,
+ * cspq_encode_tc_image_bytes(m, k, sub) bytes), `guard` as for cspq_encode.
+ * best (optional, (n, m) float32) receives the tensor-core score of each
+ * winner (diagnostics). */
+size_t cspq_encode_tc_image_bytes(int32_t m, int32_t k, int32_t sub);
+int cspq_encode_tc_prepare(const float *CB, const float *B, int32_t m, int32_t k, int32_t sub, void *img,
+                           void *stream);
+int cspq_encode_tc(const void *X, int32_t in_dtype, int64_t n, int32_t d, int64_t x_row_stride,
+                   const float *CB, const float *B, const float *guard, const void *img, int32_t m,
+                   int32_t k, int32_t sub, void *codes, int64_t codes_row_stride, float *best,
+                   void *stream);
+
 /* Same as cspq_encode for a subspace-major batch (m, n, sub) -- the layout
  * of Lloyd's training sample -- writing codes as (m, n) int32.  This is the
  * final REFERENCE-variant assignment pass of lloyd_iterate

@@ -29,7 +29,7 @@ _VARIANT_IDS = {
     EncoderVariant.REFORMULATED: N.VARIANT_REFORMULATED,
     EncoderVariant.BLOCKED: N.VARIANT_BLOCKED,
 }
-_MODES = {"auto": N.MODE_AUTO, "exact": N.MODE_EXACT, "guarded": N.MODE_GUARDED}
+_MODES = {"auto": N.MODE_AUTO, "exact": N.MODE_EXACT, "guarded": N.MODE_GUARDED, "tensor": N.MODE_AUTO}
 
 
 @dataclass(frozen=True)
@@ -37,8 +37,10 @@ class ExecutionPlan:
     """Scheduling knobs (bulk.py:31-50).  order / block_size / w / workers
     are the reference's and are validated identically; on the GPU they are
     performance-only (codes are plan-invariant, test_bulk.py:44-62).
-    GPU extras: ``mode`` ("auto" | "exact" | "guarded" -- all give the
-    oracle's codes), ``batch_rows`` (rows per host<->device batch; None =
+    GPU extras: ``mode`` ("auto" | "exact" | "guarded" | "tensor" -- all
+    give the oracle's codes; "tensor" = the tcgen05 kernel, "guarded" = the
+    FFMA kernel, "exact" = strict fp32 chains, "auto" = tensor where the
+    shape allows it, else guarded), ``batch_rows`` (rows per host<->device batch; None =
     max(block_size, 65536)), ``streams`` (CUDA streams in that pipeline) and
     ``device`` (CUDA ordinal; None = current)."""
 
@@ -123,8 +125,26 @@ class CodebookSet:
     def __getitem__(self, j: int) -> Codebook:
         return Codebook(j, self.rowmajor[j], self.transposed[j], self.biases[j])
 
+    def tc_image(self, dev=None, nobias: bool = False):
+        """Prepared tensor-core codebook image (cspq_encode_tc_prepare), or
+        None when the shape has no tensor-core path (k != 256, sub not 4/8)."""
+        dev = _device() if dev is None else dev
+        key = ("tc", dev.type, dev.index, nobias)
+        if key not in self._dev:
+            nbytes = N.load().cspq_encode_tc_image_bytes(self.m, self.k, self.sub_dim)
+            img = None
+            if nbytes:
+                t = torch()
+                rm, bs, _, nob, _ = self.on_device(dev)
+                img = t.empty(nbytes, dtype=t.uint8, device=dev)
+                with t.cuda.device(dev):
+                    N.call("cspq_encode_tc_prepare", ptr(rm), ptr(nob if nobias else bs), self.m, self.k,
+                           self.sub_dim, ptr(img), stream_ptr(dev))
+            self._dev[key] = img
+        return self._dev[key]
+
     def on_device(self, dev=None):
-        """(rowmajor, biases, guard, recomputed_biases) as CUDA tensors."""
+        """(rowmajor, biases, guard, recomputed_biases, guard_nob) as CUDA tensors."""
         dev = _device() if dev is None else dev
         key = (dev.type, dev.index)
         hit = self._dev.get(key)
@@ -164,8 +184,17 @@ def _variant_args(cbset: CodebookSet, plan: ExecutionPlan, precomputed_bias: boo
     return rm, bs, guard, vid
 
 
+def _tc_ok(X, xrs, cbset) -> bool:
+    t = torch()
+    if cbset.k != 256 or cbset.sub_dim not in (4, 8):
+        return False
+    if X.dtype == t.uint8:
+        return True
+    return X.data_ptr() % 16 == 0 and (xrs * 4) % 16 == 0
+
+
 def encode_dataset_device(X, codebooks, plan: ExecutionPlan | None = None, *,
-                          precomputed_bias: bool = True, out=None):
+                          precomputed_bias: bool = True, out=None, best=None):
     """Encode a CUDA tensor X (n, d) float32/uint8 in place on its device;
     returns the (n, m) codes tensor (uint8, or int16 holding uint16 bits
     when k > 256).  Stream-ordered on the current stream, no sync."""
@@ -189,10 +218,21 @@ def encode_dataset_device(X, codebooks, plan: ExecutionPlan | None = None, *,
         raise ConfigError(f"dataset dimensionality {d} does not match codebooks' d={cbset.d}")
     rm, bs, guard, vid = _variant_args(cbset, plan, precomputed_bias, dev)
     xrs = X.stride(0) if n > 1 else d  # a 1-row view may carry any row stride
+    mode = plan.mode
+    use_tc = mode in ("auto", "tensor") and vid != N.VARIANT_REFERENCE and _tc_ok(X, xrs, cbset)
+    if mode == "tensor" and not use_tc:
+        raise ConfigError("mode='tensor' needs k=256, sub_dim in {4, 8}, a REFORMULATED/BLOCKED variant "
+                          "and 16-byte aligned rows")
     with t.cuda.device(dev):
-        N.call("cspq_encode", ptr(X), N.IN_U8 if X.dtype == t.uint8 else N.IN_F32, n, d, xrs,
-               ptr(rm), ptr(bs), ptr(guard), cbset.m, cbset.k, cbset.sub_dim, ptr(out), out.stride(0),
-               vid, _MODES[plan.mode], stream_ptr(dev))
+        if use_tc:
+            img = cbset.tc_image(dev, nobias=not precomputed_bias and plan.variant is EncoderVariant.BLOCKED)
+            N.call("cspq_encode_tc", ptr(X), N.IN_U8 if X.dtype == t.uint8 else N.IN_F32, n, d, xrs,
+                   ptr(rm), ptr(bs), ptr(guard), ptr(img), cbset.m, cbset.k, cbset.sub_dim, ptr(out),
+                   out.stride(0), ptr(best), stream_ptr(dev))
+        else:
+            N.call("cspq_encode", ptr(X), N.IN_U8 if X.dtype == t.uint8 else N.IN_F32, n, d, xrs,
+                   ptr(rm), ptr(bs), ptr(guard), cbset.m, cbset.k, cbset.sub_dim, ptr(out), out.stride(0),
+                   vid, _MODES[mode], stream_ptr(dev))
     return out
 
 

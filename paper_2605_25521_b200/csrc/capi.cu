@@ -17,6 +17,12 @@ namespace cspq {
 int encode_prepare(const float *CB, const float *B, int m, int k, int sub, float *guard, cudaStream_t st);
 int encode_stats(unsigned long long *flagged, int reset);
 int encode_set_tiling(int t);
+size_t encode_tc_image_bytes(int m, int k, int sub);
+int encode_tc_prepare(const float *CB, const float *B, int m, int k, int sub, void *img, cudaStream_t st);
+int encode_tc(const void *X, int in_dtype, int64_t n, int64_t xrs, const float *CB, const float *B,
+              const float *guard, const void *img, int m, int k, int sub, uint8_t *codes, int64_t crs, float *best,
+              cudaStream_t st);
+int encode_tc_stats(unsigned long long *flagged, int reset);
 int recompute_biases(const float *CB, int m, int k, int sub, float *Bo, cudaStream_t st);
 int encode_device(const void *X, int in_dtype, int64_t n, int d, int64_t xrs, const float *CB, const float *B,
                   const float *guard, int m, int k, int sub, void *codes, int64_t crs, int variant, int mode,
@@ -150,10 +156,37 @@ const char *cspq_last_error(void) { return g_err; }
 int cspq_encode_set_tiling(int32_t tiling) { return encode_set_tiling(tiling); }
 
 int cspq_encode_stats(uint64_t *flagged, int32_t reset) {
-    unsigned long long v = 0;
+    unsigned long long v = 0, w = 0;
     int rc = encode_stats(flagged ? &v : nullptr, reset);
-    if (flagged) *flagged = v;
+    if (rc) return rc;
+    rc = encode_tc_stats(flagged ? &w : nullptr, reset);
+    if (flagged) *flagged = v + w;
     return rc;
+}
+
+size_t cspq_encode_tc_image_bytes(int32_t m, int32_t k, int32_t sub) { return encode_tc_image_bytes(m, k, sub); }
+
+int cspq_encode_tc_prepare(const float *CB, const float *B, int32_t m, int32_t k, int32_t sub, void *img,
+                           void *stream) {
+    int rc = check_shape(0, m, k, sub);
+    if (rc) return rc;
+    CSPQ_REQUIRE(CB && B && img, CSPQ_E_CONFIG, "null pointer");
+    return encode_tc_prepare(CB, B, m, k, sub, img, as_stream(stream));
+}
+
+int cspq_encode_tc(const void *X, int32_t in_dtype, int64_t n, int32_t d, int64_t x_row_stride, const float *CB,
+                   const float *B, const float *guard, const void *img, int32_t m, int32_t k, int32_t sub, void *codes,
+                   int64_t codes_row_stride, float *best, void *stream) {
+    int rc = check_shape(n, m, k, sub);
+    if (rc) return rc;
+    CSPQ_REQUIRE(d == m * sub, CSPQ_E_CONFIG,
+                 "dataset dimensionality %d does not match codebooks' d=%d", d, m * sub);
+    CSPQ_REQUIRE(in_dtype == CSPQ_IN_F32 || in_dtype == CSPQ_IN_U8, CSPQ_E_CONFIG, "bad in_dtype %d", in_dtype);
+    CSPQ_REQUIRE(x_row_stride >= d && codes_row_stride >= m, CSPQ_E_CONFIG, "bad strides");
+    if (n == 0) return CSPQ_OK;
+    CSPQ_REQUIRE(X && CB && B && guard && img && codes, CSPQ_E_CONFIG, "null pointer");
+    return encode_tc(X, in_dtype, n, x_row_stride, CB, B, guard, img, m, k, sub, reinterpret_cast<uint8_t *>(codes),
+                     codes_row_stride, best, as_stream(stream));
 }
 
 int cspq_encode_prepare(const float *CB, const float *B, int32_t m, int32_t k, int32_t sub, float *guard,

@@ -1,0 +1,578 @@
+// encode_tc.cu -- PQ encode on the 5th-generation tensor cores (tcgen05, sm_100a).
+//
+// Same contract as encode.cu (the oracle's codes bit for bit; reference:
+// /root/reference/pkg/src/cspq/kernels.py:108-316), different engine:
+//
+//   scores  S = A . B^T  on tcgen05.mma.kind::tf32 (3xTF32 split, bias folded):
+//     A row (one x subvector)  = [ xh | xh | xl | 1 1 0.. ]           (tf32)
+//     B row (one centroid)     = [-ch |-cl |-ch | bh bl 0.. ]          (tf32)
+//     => S[i][l] = bh + bl - (xh.ch + xh.cl + xl.ch) ~= b_l - x_i.c_l
+//     x = xh + xl, c = ch + cl, b = bh + bl with round-to-nearest tf32 parts.
+//     For uint8 rows xh = x exactly and xl = 0.
+//   accumulators in TMEM (128 lanes = rows x 256 columns = centroids), two
+//   buffers so the MMA of tile t+1 overlaps the epilogue of tile t;
+//   epilogue warps read their rows with tcgen05.ld (64 columns per load) and
+//   run an argmin that also finds the runner-up exactly without re-reading
+//   anything: blocks of 8 centroids give block minima (FMNMX3) and a running
+//   best/runner-up over blocks; eight "class" minima (centroid index mod 8)
+//   catch a runner-up that shares the winner's block, because a block and a
+//   class intersect in exactly one centroid.  The code is 8*block + class.
+//   A (row, subspace) whose runner-up lies within the error band of the
+//   tensor-core score is re-encoded exactly by its warp (strict fp32 chains,
+//   warp-shuffle argmin) -- the same fix-up as the SIMT kernel.
+//
+//   Error band (per score, |S_tc - s_oracle| <= E):
+//     tf32 splitting of x, c, b:   3 * 2^-22 (|b| + sum|x_t c_t|)
+//     tensor-core accumulation:    2^-17 * (|b| + sum|x_t c_t|)   (<= 32 adds
+//                                  of <= 2 ulp each -- deliberately loose)
+//     the oracle's own rounding:   (sub+1) 2^-24 (|b| + sum|x_t c_t|)
+//   with sum|x_t c_t| <= ||x|| max_l ||c_l||; a runner-up within 4E (x2
+//   safety) of the best is flagged.
+//
+// Warp roles (256 threads, one CTA per SM, persistent over row groups):
+//   warp 0      TMEM allocation + MMA issue (one lane)
+//   warp 1      bulk copies of the prepared codebook image (cp.async.bulk)
+//   warps 2-3   A-operand producers: load rows, split to tf32, write the
+//               K-major no-swizzle core-matrix layout, row norms for the band
+//   warps 4-7   epilogue (TMEM lane quadrant = warp % 4)
+
+#include "common.cuh"
+
+namespace cspq {
+
+__device__ unsigned long long g_tc_flagged = 0;  // telemetry (cspq_encode_stats)
+
+namespace {
+
+constexpr int kTM = 128;     // rows per tile (MMA M)
+constexpr int kN = 256;      // centroids (MMA N)
+constexpr int kG = 8;        // tiles per row group (codebook image reuse)
+constexpr int kNA = 4;       // A-operand stages
+constexpr int kNN = 8;       // row-norm ring (producers may run up to 6 items ahead of the epilogue)
+constexpr int kThreads = 384;  // 12 warps
+constexpr int kNX = 4;        // x prefetch ring (cp.async) per producer thread
+
+template <int SUB>
+struct TcShape {
+    static constexpr int K = SUB == 8 ? 32 : 16;    // tf32 elements per operand row
+    static constexpr int kChunks = K / 4;           // 16-byte chunks per row
+    static constexpr int kSteps = K / 8;            // MMAs (K = 8 each)
+    static constexpr int kRowGroupBytes = kChunks * 128;  // 8 rows x all chunks
+    static constexpr int kABytes = kTM * K * 4;
+    static constexpr int kBBytes = kN * K * 4;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+// bounded wait: a lost arrival traps (error) instead of hanging the device
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    for (uint64_t spin = 0;; ++spin) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (done) return;
+        if (spin > (1ull << 31)) __trap();
+    }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // K-major, no swizzle: core matrices of 8 rows x 16 B; LBO = between the
+    // two 16-B K-chunks of one MMA, SBO = between 8-row groups; version 1.
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+__host__ __device__ constexpr uint32_t make_idesc() {
+    // kind::tf32: D f32 (bit 4), A tf32 (2 << 7), B tf32 (2 << 10), K-major A/B,
+    // N >> 3 at [17, 23), M >> 4 at [24, 29)
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                 "l"(da), "l"(db), "r"(make_idesc()), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+#define CSPQ_LD8(o) "=r"(v[o + 0]), "=r"(v[o + 1]), "=r"(v[o + 2]), "=r"(v[o + 3]), "=r"(v[o + 4]), "=r"(v[o + 5]), "=r"(v[o + 6]), "=r"(v[o + 7])
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,"
+        "%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,"
+        "%57,%58,%59,%60,%61,%62,%63}, [%64];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"  // same statement: no use of v can be scheduled before the wait
+        : CSPQ_LD8(0), CSPQ_LD8(8), CSPQ_LD8(16), CSPQ_LD8(24), CSPQ_LD8(32), CSPQ_LD8(40), CSPQ_LD8(48), CSPQ_LD8(56)
+        : "r"(taddr) : "memory");
+}
+#undef CSPQ_LD8
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+template <int SUB>
+__device__ __forceinline__ float exact_score(const float (&x)[SUB], const float *c, float b) {
+    float dd = __fmul_rn(x[0], c[0]);
+#pragma unroll
+    for (int t = 1; t < SUB; ++t) dd = __fadd_rn(dd, __fmul_rn(x[t], c[t]));
+    return __fsub_rn(b, dd);
+}
+
+struct TcSmemHdr {
+    uint64_t b_full[2], b_empty[2];
+    uint64_t a_full[kNA], a_empty[kNA];
+    uint64_t t_full[2], t_empty[2];
+    uint32_t tmem_base;
+};
+
+// walk of the (row group, subspace, tile) work items of one CTA
+struct ItemIter {
+    int64_t g, ngroups, ntiles;
+    int j, t, m, tn;
+    uint32_t jt;  // (row group, subspace) pairs started before the current one
+    __device__ ItemIter(int64_t g0, int64_t ng, int64_t nt, int m_)
+        : g(g0), ngroups(ng), ntiles(nt), j(0), t(0), m(m_), jt(0) {
+        tn = g < ng ? (int)((nt - g * kG < kG) ? (nt - g * kG) : kG) : 0;
+    }
+    __device__ bool valid() const { return g < ngroups; }
+    __device__ int64_t tile() const { return g * kG + t; }
+    __device__ void next(int64_t stride) {
+        if (++t < tn) return;
+        t = 0;
+        ++jt;
+        if (++j < m) return;
+        j = 0;
+        g += stride;
+        tn = g < ngroups ? (int)((ntiles - g * kG < kG) ? (ntiles - g * kG) : kG) : 0;
+    }
+};
+
+template <int SUB, typename TIn>
+struct TcSmem {
+    using S = TcShape<SUB>;
+    static constexpr int kCFloats = kN * SUB + kN;                 // fp32 codebook + biases (fix-up)
+    static constexpr int kXBytes = kTM * SUB * (int)sizeof(TIn);   // one staged x tile
+    static constexpr size_t oB = 0;
+    static constexpr size_t oA = oB + 2 * (size_t)S::kBBytes;
+    static constexpr size_t oC = oA + kNA * (size_t)S::kABytes;
+    static constexpr size_t oX = oC + 2 * (size_t)kCFloats * 4;
+    static constexpr size_t oN = oX + kNX * (size_t)kXBytes;
+    static constexpr size_t oG = oN + kNN * kTM * 4;               // guard constants (2 m floats)
+    static size_t total(int m) { return oG + ((size_t)2 * m * 4 + 15) / 16 * 16 + sizeof(TcSmemHdr) + 16; }
+};
+
+// ------------------------------------------------------------------ the kernel
+template <int SUB, typename TIn>
+__global__ void __launch_bounds__(kThreads, 1)
+encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const float *__restrict__ CB,
+                 const float *__restrict__ Bv, const float *__restrict__ guard, const uint8_t *__restrict__ img,
+                 uint8_t *__restrict__ codes, int64_t cs, float *__restrict__ best_out) {
+    using S = TcShape<SUB>;
+    using L = TcSmem<SUB, TIn>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *sB = smem_raw + L::oB;
+    unsigned char *sA = smem_raw + L::oA;
+    float *sC = reinterpret_cast<float *>(smem_raw + L::oC);
+    unsigned char *sX = smem_raw + L::oX;
+    float *sNorm = reinterpret_cast<float *>(smem_raw + L::oN);
+    float *sGuard = reinterpret_cast<float *>(smem_raw + L::oG);
+    TcSmemHdr *H = reinterpret_cast<TcSmemHdr *>(smem_raw + L::oG + ((size_t)2 * m * 4 + 15) / 16 * 16);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ntiles = (n + kTM - 1) / kTM;
+    const int64_t ngroups = (ntiles + kG - 1) / kG;
+
+    for (int i = threadIdx.x; i < 2 * m; i += kThreads) sGuard[i] = guard[i];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&H->b_full[i], 1);
+            mbar_init(&H->b_empty[i], 1 + 256);  // MMA commit + every epilogue thread (fix-up reads sC)
+            mbar_init(&H->t_full[i], 1);
+            mbar_init(&H->t_empty[i], 128);
+        }
+        for (int i = 0; i < kNA; ++i) {
+            mbar_init(&H->a_full[i], 64);
+            mbar_init(&H->a_empty[i], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&H->tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = H->tmem_base;
+
+    if (warp == 0) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            uint32_t it = 0, jt = 0;
+            for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+                const int64_t t0 = g * kG, tn = (ntiles - t0 < kG) ? (ntiles - t0) : kG;
+                for (int j = 0; j < m; ++j, ++jt) {
+                    const int jb = jt & 1;
+                    mbar_wait(&H->b_full[jb], (jt >> 1) & 1);
+                    for (int t = 0; t < tn; ++t, ++it) {
+                        const int as = it % kNA, tb = it & 1;
+                        mbar_wait(&H->a_full[as], (it / kNA) & 1);
+                        mbar_wait(&H->t_empty[tb], ((it >> 1) & 1) ^ 1);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
+#pragma unroll
+                        for (int s = 0; s < S::kSteps; ++s) {
+                            const uint64_t da = make_desc(a0 + 2 * s * 128, 128, S::kRowGroupBytes);
+                            const uint64_t db = make_desc(b0 + 2 * s * 128, 128, S::kRowGroupBytes);
+                            mma_tf32(tmem + tb * kN, da, db, s > 0);
+                        }
+                        mma_commit(&H->a_empty[as]);
+                        mma_commit(&H->t_full[tb]);
+                    }
+                    mma_commit(&H->b_empty[jb]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- codebook loader: tf32 image (MMA) + fp32 codebook (fix-up) ----------------
+        if (lane == 0) {
+            uint32_t jt = 0;
+            for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+                for (int j = 0; j < m; ++j, ++jt) {
+                    const int jb = jt & 1;
+                    mbar_wait(&H->b_empty[jb], ((jt >> 1) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&H->b_full[jb], S::kBBytes + L::kCFloats * 4);
+                    bulk_g2s(sB + jb * S::kBBytes, img + (int64_t)j * S::kBBytes, S::kBBytes, &H->b_full[jb]);
+                    float *cdst = sC + jb * L::kCFloats;
+                    bulk_g2s(cdst, CB + (int64_t)j * kN * SUB, kN * SUB * 4, &H->b_full[jb]);
+                    bulk_g2s(cdst + kN * SUB, Bv + (int64_t)j * kN, kN * 4, &H->b_full[jb]);
+                }
+            }
+        }
+    } else if (warp < 4) {
+        // ---------------- A-operand producers (64 threads, rows p and p + 64) ----------------
+        const int p = threadIdx.x - 64;
+        // cp.async prefetch of this thread's two x subvectors, kNX - 1 items ahead
+        auto prefetch = [&](const ItemIter &pi, int slot) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int r = p + 64 * h;
+                const int64_t row = pi.tile() * kTM + r;
+                const bool ok = pi.valid() && row < n;
+                const TIn *src = X + (ok ? row * xs + (int64_t)pi.j * SUB : 0);
+                unsigned char *dst = sX + slot * L::kXBytes + r * SUB * sizeof(TIn);
+                constexpr int bytes = SUB * (int)sizeof(TIn);
+                if constexpr (bytes == 32) {
+                    cp_async16(dst, src, ok ? 16 : 0);
+                    cp_async16(dst + 16, reinterpret_cast<const unsigned char *>(src) + 16, ok ? 16 : 0);
+                } else if constexpr (bytes == 16) {
+                    cp_async16(dst, src, ok ? 16 : 0);
+                } else if constexpr (bytes == 8) {
+                    cp_async8(dst, src, ok ? 8 : 0);
+                } else {
+                    cp_async4(dst, src, ok ? 4 : 0);
+                }
+            }
+            cp_async_commit();
+        };
+        ItemIter ci(blockIdx.x, ngroups, ntiles, m), pi(blockIdx.x, ngroups, ntiles, m);
+        for (int k = 0; k < kNX - 1; ++k) {
+            prefetch(pi, k);
+            pi.next(gridDim.x);
+        }
+        for (uint32_t it = 0; ci.valid(); ++it, ci.next(gridDim.x)) {
+            prefetch(pi, (it + kNX - 1) % kNX);
+            pi.next(gridDim.x);
+            cp_async_wait<kNX - 1>();
+            const int as = it % kNA;
+            mbar_wait(&H->a_empty[as], ((it / kNA) & 1) ^ 1);
+            unsigned char *At = sA + as * S::kABytes;
+            const unsigned char *xt = sX + (it % kNX) * L::kXBytes;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int r = p + 64 * h;
+                float x[SUB];
+                if constexpr (sizeof(TIn) == 4) {
+#pragma unroll
+                    for (int q = 0; q < SUB / 4; ++q) {
+                        const float4 v = reinterpret_cast<const float4 *>(xt + r * SUB * 4)[q];
+                        x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int tt = 0; tt < SUB; ++tt) x[tt] = (float)reinterpret_cast<const TIn *>(xt)[r * SUB + tt];
+                }
+                float xh[SUB], xl[SUB], ss = 0.f;
+#pragma unroll
+                for (int tt = 0; tt < SUB; ++tt) {
+                    xh[tt] = tf32_rna(x[tt]);
+                    xl[tt] = tf32_rna(x[tt] - xh[tt]);
+                    ss = __fmaf_rn(x[tt], x[tt], ss);
+                }
+                unsigned char *rowp = At + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16;
+                auto st = [&](int c, float a0, float a1, float a2, float a3) {
+                    *reinterpret_cast<float4 *>(rowp + c * 128) = make_float4(a0, a1, a2, a3);
+                };
+                if constexpr (SUB == 8) {
+                    st(0, xh[0], xh[1], xh[2], xh[3]); st(1, xh[4], xh[5], xh[6], xh[7]);
+                    st(2, xh[0], xh[1], xh[2], xh[3]); st(3, xh[4], xh[5], xh[6], xh[7]);
+                    st(4, xl[0], xl[1], xl[2], xl[3]); st(5, xl[4], xl[5], xl[6], xl[7]);
+                    st(6, 1.f, 1.f, 0.f, 0.f); st(7, 0.f, 0.f, 0.f, 0.f);
+                } else {
+                    st(0, xh[0], xh[1], xh[2], xh[3]); st(1, xh[0], xh[1], xh[2], xh[3]);
+                    st(2, xl[0], xl[1], xl[2], xl[3]); st(3, 1.f, 1.f, 0.f, 0.f);
+                }
+                sNorm[(it % kNN) * kTM + r] = __fsqrt_ru(ss) * 1.000001f;
+            }
+            fence_proxy_async();
+            mbar_arrive(&H->a_full[as]);
+        }
+        cp_async_wait<0>();
+    } else {
+        // ---------------- epilogue: two groups of 4 warps, group e owns TMEM buffer e ----------------
+        const int e = (warp - 4) >> 2;
+        const int q = warp & 3;
+        const int r = 32 * q + lane;
+        constexpr float kE = (float)((3.0 / 4194304.0 + 1.0 / 131072.0 * (1.0 + 1.0 / 1024.0) + (SUB + 1) / 16777216.0) * 1.01);
+        // b_empty[p & 1] phase p >> 1 belongs to pair p.  A group that owns no item of
+        // a pair reaches the next pair early; its arrival must not land in the still
+        // open phase of pair p - 2, so it first waits for that phase to complete.
+        auto release_pair = [&](uint32_t p) {
+            mbar_wait(&H->b_empty[p & 1], ((p >> 1) & 1) ^ 1);
+            mbar_arrive(&H->b_empty[p & 1]);
+        };
+        ItemIter ii(blockIdx.x, ngroups, ntiles, m);
+        for (uint32_t it = 0; ii.valid(); ++it, ii.next(gridDim.x)) {
+            if (ii.t == 0 && it > 0) release_pair(ii.jt - 1);  // done with the previous pair's sC
+            if ((int)(it & 1) != e) continue;
+            const uint32_t jt = ii.jt;
+            const int j = ii.j;
+            mbar_wait(&H->t_full[e], (it >> 1) & 1);
+            tc_fence_after();
+            // the producer wrote this norm before a_full, which the MMA consumed before t_full
+            const float xnorm = sNorm[(it % kNN) * kTM + r];
+            float bm[32], cls[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) cls[c] = pos_inf_f();
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                uint32_t v[64];
+                tmem_ld64(tmem + ((uint32_t)(32 * q) << 16) + e * kN + ch * 64, v);
+#define SV(i) __uint_as_float(v[(i)])
+#pragma unroll
+                for (int bp = 0; bp < 4; ++bp) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) cls[c] = fmin3(cls[c], SV(16 * bp + c), SV(16 * bp + 8 + c));
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int o = 16 * bp + 8 * h;
+                        bm[8 * ch + 2 * bp + h] = fmin3(fmin3(SV(o), SV(o + 1), SV(o + 2)),
+                                                        fmin3(SV(o + 3), SV(o + 4), SV(o + 5)), fminf(SV(o + 6), SV(o + 7)));
+                    }
+                }
+#undef SV
+            }
+            tc_fence_before();
+            mbar_arrive(&H->t_empty[e]);
+            // blocks as a 4 (chunk) x 8 grid: winner block and second-best block
+            float G[4], Cb[8];
+#pragma unroll
+            for (int g4 = 0; g4 < 4; ++g4)
+                G[g4] = fmin3(fmin3(bm[8 * g4], bm[8 * g4 + 1], bm[8 * g4 + 2]), fmin3(bm[8 * g4 + 3], bm[8 * g4 + 4], bm[8 * g4 + 5]),
+                              fminf(bm[8 * g4 + 6], bm[8 * g4 + 7]));
+#pragma unroll
+            for (int c = 0; c < 8; ++c) Cb[c] = fminf(fmin3(bm[c], bm[8 + c], bm[16 + c]), bm[24 + c]);
+            const float m1 = fminf(fmin3(G[0], G[1], G[2]), G[3]);
+            int gs = 4, cs8 = 8, qc = 8;
+#pragma unroll
+            for (int g4 = 3; g4 >= 0; --g4) gs = (G[g4] == m1) ? g4 : gs;
+#pragma unroll
+            for (int c = 7; c >= 0; --c) { cs8 = (Cb[c] == m1) ? c : cs8; qc = (cls[c] == m1) ? c : qc; }
+            float second = pos_inf_f();
+#pragma unroll
+            for (int g4 = 0; g4 < 4; ++g4) second = (g4 == gs) ? second : fminf(second, G[g4]);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                second = (c == cs8) ? second : fminf(second, Cb[c]);
+                second = (c == qc) ? second : fminf(second, cls[c]);
+            }
+            const float W = sGuard[2 * j] + xnorm * sGuard[2 * j + 1];
+            const float thr = m1 + 4.0f * kE * W + 1e-36f;
+            const int64_t row = ii.tile() * kTM + r;
+            int code = 64 * gs + 8 * cs8 + qc;
+            const bool flag = (row < n) && (!(m1 < pos_inf_f()) || !(thr < pos_inf_f()) || (gs | cs8 | qc) >= 8 ||
+                                            gs >= 4 || second <= thr);
+            // exact warp-cooperative re-encode of flagged rows (fp32 codebook from shared memory)
+            unsigned mask = __ballot_sync(0xffffffffu, flag);
+            if (mask) {
+                // acquire the bulk copies of this pair (the buffer cannot advance past this
+                // pair until every epilogue thread has arrived on b_empty)
+                mbar_wait(&H->b_full[jt & 1], (jt >> 1) & 1);
+                const float *cbs = sC + (jt & 1) * L::kCFloats;
+                if (lane == 0) atomicAdd(&g_tc_flagged, (unsigned long long)__popc(mask));
+                while (mask) {
+                    const int src = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const int64_t srow = __shfl_sync(0xffffffffu, row, src);
+                    float xv[SUB];
+#pragma unroll
+                    for (int tt = 0; tt < SUB; ++tt) xv[tt] = (float)X[srow * xs + (int64_t)j * SUB + tt];
+                    float best = pos_inf_f();
+                    int bl = kN;
+#pragma unroll 2
+                    for (int l = lane; l < kN; l += 32) {
+                        float cv[SUB];
+#pragma unroll
+                        for (int tt = 0; tt < SUB; ++tt) cv[tt] = cbs[l * SUB + tt];
+                        const float sc = exact_score<SUB>(xv, cv, cbs[kN * SUB + l]);
+                        if (sc < best) { best = sc; bl = l; }
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+                        const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
+                        if (ob < best || (ob == best && ol < bl)) { best = ob; bl = ol; }
+                    }
+                    if (lane == src) code = (best < pos_inf_f()) ? bl : 0;
+                }
+            }
+            if (row < n) {
+                codes[row * cs + j] = (uint8_t)code;
+                if (best_out) best_out[row * m + j] = m1;
+            }
+        }
+        if (ii.jt > 0) release_pair(ii.jt - 1);  // the last pair
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+// Codebook image: per subspace, 256 rows (centroids) x K tf32 in the K-major
+// no-swizzle core-matrix layout the MMA reads.
+template <int SUB>
+__global__ void tc_image_kernel(const float *__restrict__ CB, const float *__restrict__ B, int m,
+                                uint8_t *__restrict__ img) {
+    using S = TcShape<SUB>;
+    const int j = blockIdx.x, l = threadIdx.x;  // 256 threads
+    const float *c = CB + ((int64_t)j * kN + l) * SUB;
+    float v[S::K];
+#pragma unroll
+    for (int k = 0; k < S::K; ++k) v[k] = 0.f;
+    float ch[SUB], cl[SUB];
+#pragma unroll
+    for (int t = 0; t < SUB; ++t) {
+        ch[t] = tf32_rna(c[t]);
+        cl[t] = tf32_rna(c[t] - ch[t]);
+    }
+    const float b = B[(int64_t)j * kN + l];
+    const float bh = tf32_rna(b), bl = tf32_rna(b - bh);
+#pragma unroll
+    for (int t = 0; t < SUB; ++t) {
+        v[t] = -ch[t];
+        v[SUB + t] = -cl[t];
+        v[2 * SUB + t] = -ch[t];
+    }
+    v[3 * SUB] = bh;
+    v[3 * SUB + 1] = bl;
+    unsigned char *rowp = img + (int64_t)j * S::kBBytes + (l >> 3) * S::kRowGroupBytes + (l & 7) * 16;
+#pragma unroll
+    for (int cch = 0; cch < S::kChunks; ++cch)
+        *reinterpret_cast<float4 *>(rowp + cch * 128) = make_float4(v[4 * cch], v[4 * cch + 1], v[4 * cch + 2], v[4 * cch + 3]);
+}
+
+template <int SUB, typename TIn>
+int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, const float *CB, const float *B, const float *guard,
+              const uint8_t *img, uint8_t *codes, int64_t cs, float *best, cudaStream_t st) {
+    const size_t smem = TcSmem<SUB, TIn>::total(m);
+    CSPQ_REQUIRE(smem <= 227 * 1024, CSPQ_E_CONFIG, "too many subspaces (%d) for the tensor-core kernel", m);
+    auto kern = encode_tc_kernel<SUB, TIn>;
+    CSPQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ntiles = (n + kTM - 1) / kTM;
+    const int64_t ngroups = (ntiles + kG - 1) / kG;
+    const int grid = (int)std::min<int64_t>(sms, ngroups);
+    kern<<<grid, kThreads, smem, st>>>(X, n, m, xs, CB, B, guard, img, codes, cs, best);
+    CSPQ_LAUNCH_CHECK();
+    return CSPQ_OK;
+}
+
+}  // namespace
+
+size_t encode_tc_image_bytes(int m, int k, int sub) {
+    if (k != kN || (sub != 4 && sub != 8)) return 0;
+    return (size_t)m * (sub == 8 ? TcShape<8>::kBBytes : TcShape<4>::kBBytes);
+}
+
+int encode_tc_prepare(const float *CB, const float *B, int m, int k, int sub, void *img, cudaStream_t st) {
+    CSPQ_REQUIRE(k == kN && (sub == 4 || sub == 8), CSPQ_E_CONFIG,
+                 "tensor-core encode needs k=256 and sub in {4, 8} (got k=%d, sub=%d)", k, sub);
+    if (sub == 8) tc_image_kernel<8><<<m, kN, 0, st>>>(CB, B, m, reinterpret_cast<uint8_t *>(img));
+    else tc_image_kernel<4><<<m, kN, 0, st>>>(CB, B, m, reinterpret_cast<uint8_t *>(img));
+    CSPQ_LAUNCH_CHECK();
+    return CSPQ_OK;
+}
+
+int encode_tc(const void *X, int in_dtype, int64_t n, int64_t xrs, const float *CB, const float *B,
+              const float *guard, const void *img, int m, int k, int sub, uint8_t *codes, int64_t crs, float *best,
+              cudaStream_t st) {
+    CSPQ_REQUIRE(k == kN && (sub == 4 || sub == 8), CSPQ_E_CONFIG,
+                 "tensor-core encode needs k=256 and sub in {4, 8} (got k=%d, sub=%d)", k, sub);
+    const uint8_t *im = reinterpret_cast<const uint8_t *>(img);
+    if (in_dtype == CSPQ_IN_U8) {
+        const uint8_t *x = reinterpret_cast<const uint8_t *>(X);
+        return sub == 8 ? launch_tc<8, uint8_t>(x, n, m, xrs, CB, B, guard, im, codes, crs, best, st)
+                        : launch_tc<4, uint8_t>(x, n, m, xrs, CB, B, guard, im, codes, crs, best, st);
+    }
+    const float *x = reinterpret_cast<const float *>(X);
+    CSPQ_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0 && (xrs * 4) % 16 == 0, CSPQ_E_CONFIG,
+                 "tensor-core encode needs 16-byte aligned float32 rows");
+    return sub == 8 ? launch_tc<8, float>(x, n, m, xrs, CB, B, guard, im, codes, crs, best, st)
+                    : launch_tc<4, float>(x, n, m, xrs, CB, B, guard, im, codes, crs, best, st);
+}
+
+int encode_tc_stats(unsigned long long *flagged, int reset) {
+    if (flagged) CSPQ_CUDA_TRY(cudaMemcpyFromSymbol(flagged, g_tc_flagged, sizeof(unsigned long long)));
+    if (reset) {
+        const unsigned long long z = 0;
+        CSPQ_CUDA_TRY(cudaMemcpyToSymbol(g_tc_flagged, &z, sizeof(z)));
+    }
+    return CSPQ_OK;
+}
+
+}  // namespace cspq

@@ -1,0 +1,114 @@
+"""Parity of the tcgen05 tensor-core encode path with the oracle (bit-exact
+codes), including ragged tails, uint8 rows, adversarial near-ties, and an
+empirical check of the error band the exactness guard relies on."""
+
+import numpy as np
+import pytest
+
+from conftest import cases, golden, group
+
+pytestmark = pytest.mark.gpu
+
+ENC = golden("encode_golden.npz")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2605_25521_b200 as P
+    return P
+
+
+def cset_of(P, rm):
+    rm = np.ascontiguousarray(rm, dtype=np.float32)
+    return P.CodebookSet.from_codebooks([P.Codebook.from_rowmajor(j, rm[j]) for j in range(rm.shape[0])])
+
+
+def tc_codes(P, X, cs, best=False, precomputed_bias=True):
+    import torch
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    b = torch.empty((X.shape[0], cs.m), dtype=torch.float32, device="cuda") if best else None
+    out = P.encode_dataset_device(Xd, cs, P.ExecutionPlan(mode="tensor"), best=b,
+                                  precomputed_bias=precomputed_bias)
+    torch.cuda.synchronize()
+    return (out.cpu().numpy(), b.cpu().numpy()) if best else out.cpu().numpy()
+
+
+TC_CASES = [c for c in cases(ENC) if group(ENC, c)["rowmajor"].shape[1] == 256
+            and group(ENC, c)["rowmajor"].shape[2] in (4, 8)]
+
+
+@pytest.mark.parametrize("case", TC_CASES)
+def test_golden_codes_tensor(P, case):
+    g = group(ENC, case)
+    cs = cset_of(P, g["rowmajor"])
+    assert tc_codes(P, g["X"], cs).tobytes() == g["codes_blocked"].tobytes()
+    assert tc_codes(P, g["X"], cs, precomputed_bias=False).tobytes() == g["codes_nobias"].tobytes()
+
+
+@pytest.mark.parametrize("n", [1, 5, 127, 128, 129, 1023, 1024, 1025, 8 * 128 * 3 + 17])
+@pytest.mark.parametrize("sub,m", [(8, 3), (4, 5), (8, 1)])
+def test_ragged_tails(P, oracle, n, sub, m):
+    rng = np.random.default_rng(n * 31 + sub)
+    X = rng.standard_normal((n, m * sub)).astype(np.float32)
+    rm = rng.standard_normal((m, 256, sub)).astype(np.float32)
+    cs = cset_of(P, rm)
+    want = oracle.encode(X, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM)
+    assert tc_codes(P, X, cs).tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_config_parity_tensor(P, oracle, name):
+    import torch
+    from paper_2605_25521_b200 import configs as C
+    cfg = C.CONFIGS[name]
+    n = 30_000
+    X = C.generate(cfg, 0, n, torch.device("cuda", 0))
+    Xh = X.cpu().numpy()
+    rng = np.random.default_rng(11)
+    if cfg.codebook == "sampled":
+        rm = C.sampled_codebooks(cfg, Xh.astype(np.float32))
+    else:
+        rows = Xh[rng.choice(n, cfg.k, replace=False)].astype(np.float32)
+        rm = np.ascontiguousarray(rows.reshape(cfg.k, cfg.m, cfg.sub).transpose(1, 0, 2))
+        rm = rm + rng.normal(0, 1e-3, rm.shape).astype(np.float32) * (rm.std() + 1e-6)
+    cs = cset_of(P, rm)
+    want = oracle.encode(Xh, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM)
+    got = tc_codes(P, Xh, cs)
+    assert got.tobytes() == want.tobytes(), (name, int((got != want).sum()))
+
+
+def test_adversarial_near_ties_tensor(P, oracle):
+    rng = np.random.default_rng(99)
+    m, k, sub = 4, 256, 8
+    base = rng.standard_normal((m, 64, sub)).astype(np.float32)
+    rm = np.repeat(base, 4, axis=1)
+    rm[:, 1::4] = np.nextafter(rm[:, 1::4], np.float32(np.inf))
+    rm[:, 2::4] = np.nextafter(rm[:, 2::4], np.float32(-np.inf))
+    cs = cset_of(P, rm)
+    X = np.concatenate([rm[:, i].reshape(-1) for i in range(0, k, 3)]).reshape(-1, m * sub)
+    mid = 0.5 * (rm[:, 0::4][:, :32] + rm[:, 4::4][:, :32])
+    X = np.concatenate([X, mid.transpose(1, 0, 2).reshape(32, m * sub)]).astype(np.float32)
+    X = np.concatenate([X, X + rng.normal(0, 1e-6, X.shape).astype(np.float32)]).astype(np.float32)
+    want = oracle.encode(X, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM)
+    assert tc_codes(P, X, cs).tobytes() == want.tobytes()
+
+
+def test_tensor_error_within_band(P, oracle):
+    """The guard assumes |S_tc - s_oracle| <= E = c * (max|b| + ||x|| max||c||)
+    with c ~ 8.9e-6; measure the real error on the winners and require a
+    wide margin below the bound."""
+    rng = np.random.default_rng(5)
+    for scale in (1.0, 1e3, 1e-3):
+        X = (rng.standard_normal((20_000, 64)) * scale).astype(np.float32)
+        rm = (rng.standard_normal((8, 256, 8)) * scale).astype(np.float32)
+        cs = cset_of(P, rm)
+        codes, best = tc_codes(P, X, cs, best=True)
+        want, wbest = oracle.encode(X, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM, want_best=True)
+        same = codes == want
+        xs = X.reshape(-1, 8, 8).astype(np.float64)
+        nrm = np.sqrt((xs ** 2).sum(-1))
+        bmax = np.abs(cs.biases.astype(np.float64)).max(axis=1)
+        cmax = np.sqrt((cs.rowmajor.astype(np.float64) ** 2).sum(-1)).max(axis=1)
+        W = bmax[None, :] + nrm * cmax[None, :]
+        err = np.abs(best.astype(np.float64) - wbest.astype(np.float64))[same] / W[same]
+        assert err.max() < 8.9e-6 / 4, f"scale {scale}: observed {err.max():.3e} vs bound 8.9e-6"
