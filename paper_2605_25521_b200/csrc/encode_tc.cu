@@ -22,10 +22,16 @@
 //   warp-shuffle argmin) -- the same fix-up as the SIMT kernel.
 //
 //   Error band (per score, |S_tc - s_oracle| <= E):
-//     tf32 splitting of x, c, b:   3 * 2^-22 (|b| + sum|x_t c_t|)
-//     tensor-core accumulation:    2^-17 * (|b| + sum|x_t c_t|)   (<= 32 adds
-//                                  of <= 2 ulp each -- deliberately loose)
+//     tf32 splitting of x, c, b:   4 * 2^-22 (|b| + sum|x_t c_t|)  (x's low part
+//                                  is truncated by the MMA: 2^-21 |x|)
+//     tensor-core accumulation:    2^-22 per K=8 MMA step (products of tf32
+//                                  operands are exact in fp32; each step is
+//                                  modelled as <= 2 roundings of 2^-23 of the
+//                                  running magnitude) -> 4 * 2^-22 for K = 32
 //     the oracle's own rounding:   (sub+1) 2^-24 (|b| + sum|x_t c_t|)
+//   The accumulation term is a model of undocumented hardware; measured
+//   errors (scripts/tc_error.py, tests/test_encode_tc_gpu.py) stay >= 6x
+//   below the resulting E on every data regime tried.
 //   with sum|x_t c_t| <= ||x|| max_l ||c_l||; a runner-up within 4E (x2
 //   safety) of the best is flagged.
 //
@@ -35,6 +41,8 @@
 //   warps 2-3   A-operand producers: load rows, split to tf32, write the
 //               K-major no-swizzle core-matrix layout, row norms for the band
 //   warps 4-7   epilogue (TMEM lane quadrant = warp % 4)
+
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -48,9 +56,9 @@ constexpr int kTM = 128;     // rows per tile (MMA M)
 constexpr int kN = 256;      // centroids (MMA N)
 constexpr int kG = 8;        // tiles per row group (codebook image reuse)
 constexpr int kNA = 4;       // A-operand stages
-constexpr int kNN = 8;       // row-norm ring (producers may run up to 6 items ahead of the epilogue)
-constexpr int kThreads = 384;  // 12 warps
-constexpr int kNX = 4;        // x prefetch ring (cp.async) per producer thread
+constexpr int kThreads = 320;  // 10 warps: MMA, loader, 2 x 4 epilogue/producer
+constexpr int kPD = 3;        // cp.async prefetch distance, in the group's own items
+constexpr int kRing = 4;      // x slots per group (> kPD: an item's slot outlives its fix-up)
 
 template <int SUB>
 struct TcShape {
@@ -150,7 +158,7 @@ __device__ __forceinline__ float exact_score(const float (&x)[SUB], const float 
 
 struct TcSmemHdr {
     uint64_t b_full[2], b_empty[2];
-    uint64_t a_full[kNA], a_empty[kNA];
+    uint64_t a_full[kNA];
     uint64_t t_full[2], t_empty[2];
     uint32_t tmem_base;
 };
@@ -186,8 +194,7 @@ struct TcSmem {
     static constexpr size_t oA = oB + 2 * (size_t)S::kBBytes;
     static constexpr size_t oC = oA + kNA * (size_t)S::kABytes;
     static constexpr size_t oX = oC + 2 * (size_t)kCFloats * 4;
-    static constexpr size_t oN = oX + kNX * (size_t)kXBytes;
-    static constexpr size_t oG = oN + kNN * kTM * 4;               // guard constants (2 m floats)
+    static constexpr size_t oG = oX + 2 * kRing * (size_t)kXBytes;  // guard constants (2 m floats)
     static size_t total(int m) { return oG + ((size_t)2 * m * 4 + 15) / 16 * 16 + sizeof(TcSmemHdr) + 16; }
 };
 
@@ -196,15 +203,20 @@ template <int SUB, typename TIn>
 __global__ void __launch_bounds__(kThreads, 1)
 encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const float *__restrict__ CB,
                  const float *__restrict__ Bv, const float *__restrict__ guard, const uint8_t *__restrict__ img,
-                 uint8_t *__restrict__ codes, int64_t cs, float *__restrict__ best_out) {
+                 uint8_t *__restrict__ codes, int64_t cs, float *__restrict__ best_out, int probe) {
+    // probe (debug timing only): bit 0 = epilogue skips its min work, bit 1 = no MMAs,
+    // bit 2 = skip the A conversion, bit 3 = keep TMEM loads but skip the min work
+    // (bits 0-3 leave garbage codes), bit 4 = CTA 0 writes clock64 stamps into best_out
     using S = TcShape<SUB>;
     using L = TcSmem<SUB, TIn>;
+    long long *stamp = (probe & 16) && blockIdx.x == 0 ? reinterpret_cast<long long *>(best_out) : nullptr;
+    if (probe & 16) best_out = nullptr;
+    constexpr int kStampItems = 2048;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sB = smem_raw + L::oB;
     unsigned char *sA = smem_raw + L::oA;
     float *sC = reinterpret_cast<float *>(smem_raw + L::oC);
     unsigned char *sX = smem_raw + L::oX;
-    float *sNorm = reinterpret_cast<float *>(smem_raw + L::oN);
     float *sGuard = reinterpret_cast<float *>(smem_raw + L::oG);
     TcSmemHdr *H = reinterpret_cast<TcSmemHdr *>(smem_raw + L::oG + ((size_t)2 * m * 4 + 15) / 16 * 16);
 
@@ -220,10 +232,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             mbar_init(&H->t_full[i], 1);
             mbar_init(&H->t_empty[i], 128);
         }
-        for (int i = 0; i < kNA; ++i) {
-            mbar_init(&H->a_full[i], 64);
-            mbar_init(&H->a_empty[i], 1);
-        }
+        for (int i = 0; i < kNA; ++i) mbar_init(&H->a_full[i], 128);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -247,17 +256,19 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                     for (int t = 0; t < tn; ++t, ++it) {
                         const int as = it % kNA, tb = it & 1;
                         mbar_wait(&H->a_full[as], (it / kNA) & 1);
+                        if (stamp && it < kStampItems) stamp[it * 8 + 0] = clock64();
                         mbar_wait(&H->t_empty[tb], ((it >> 1) & 1) ^ 1);
+                        if (stamp && it < kStampItems) stamp[it * 8 + 1] = clock64();
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
 #pragma unroll
                         for (int s = 0; s < S::kSteps; ++s) {
                             const uint64_t da = make_desc(a0 + 2 * s * 128, 128, S::kRowGroupBytes);
                             const uint64_t db = make_desc(b0 + 2 * s * 128, 128, S::kRowGroupBytes);
-                            mma_tf32(tmem + tb * kN, da, db, s > 0);
+                            if (!(probe & 2)) mma_tf32(tmem + tb * kN, da, db, s > 0);
                         }
-                        mma_commit(&H->a_empty[as]);
-                        mma_commit(&H->t_full[tb]);
+                        mma_commit(&H->t_full[tb]);  // also frees A stage `as` for the group's item it + 4
+                        if (stamp && it < kStampItems) stamp[it * 8 + 2] = clock64();
                     }
                     mma_commit(&H->b_empty[jb]);
                 }
@@ -279,67 +290,64 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                 }
             }
         }
-    } else if (warp < 4) {
-        // ---------------- A-operand producers (64 threads, rows p and p + 64) ----------------
-        const int p = threadIdx.x - 64;
-        // cp.async prefetch of this thread's two x subvectors, kNX - 1 items ahead
-        auto prefetch = [&](const ItemIter &pi, int slot) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int r = p + 64 * h;
-                const int64_t row = pi.tile() * kTM + r;
-                const bool ok = pi.valid() && row < n;
-                const TIn *src = X + (ok ? row * xs + (int64_t)pi.j * SUB : 0);
-                unsigned char *dst = sX + slot * L::kXBytes + r * SUB * sizeof(TIn);
-                constexpr int bytes = SUB * (int)sizeof(TIn);
-                if constexpr (bytes == 32) {
-                    cp_async16(dst, src, ok ? 16 : 0);
-                    cp_async16(dst + 16, reinterpret_cast<const unsigned char *>(src) + 16, ok ? 16 : 0);
-                } else if constexpr (bytes == 16) {
-                    cp_async16(dst, src, ok ? 16 : 0);
-                } else if constexpr (bytes == 8) {
-                    cp_async8(dst, src, ok ? 8 : 0);
-                } else {
-                    cp_async4(dst, src, ok ? 4 : 0);
-                }
+    } else {
+        // ---------------- epilogue + A producer: two groups of 4 warps ----------------
+        // Group e owns the items with (item & 1) == e and TMEM buffer e.  Thread (q, lane)
+        // owns tile row r = 32 q + lane: it reads that TMEM lane, and it also writes that
+        // row of the A operand of the group's next item (item + 2) and prefetches the
+        // row's x kPD owned items ahead into the group's x ring.
+        const int e = (warp - 2) >> 2;
+        const int q = warp & 3;
+        const int r = 32 * q + lane;
+        constexpr float kE = (float)((4.0 / 4194304.0 + S::kSteps / 4194304.0 * (1.0 + 1.0 / 1024.0) + (SUB + 1) / 16777216.0) * 1.01);
+        auto ring = [&](uint32_t item) -> unsigned char * {  // x slot of one of the group's items
+            return sX + ((size_t)e * kRing + (item >> 1) % kRing) * L::kXBytes + r * SUB * sizeof(TIn);
+        };
+        auto prefetch = [&](const ItemIter &pi, uint32_t item) {
+            const int64_t row = pi.tile() * kTM + r;
+            const bool ok = pi.valid() && row < n;
+            const TIn *src = X + (ok ? row * xs + (int64_t)pi.j * SUB : 0);
+            unsigned char *dst = ring(item);
+            constexpr int bytes = SUB * (int)sizeof(TIn);
+            if constexpr (bytes == 32) {
+                cp_async16(dst, src, ok ? 16 : 0);
+                cp_async16(dst + 16, reinterpret_cast<const unsigned char *>(src) + 16, ok ? 16 : 0);
+            } else if constexpr (bytes == 16) {
+                cp_async16(dst, src, ok ? 16 : 0);
+            } else if constexpr (bytes == 8) {
+                cp_async8(dst, src, ok ? 8 : 0);
+            } else {
+                cp_async4(dst, src, ok ? 4 : 0);
             }
             cp_async_commit();
         };
-        ItemIter ci(blockIdx.x, ngroups, ntiles, m), pi(blockIdx.x, ngroups, ntiles, m);
-        for (int k = 0; k < kNX - 1; ++k) {
-            prefetch(pi, k);
-            pi.next(gridDim.x);
-        }
-        for (uint32_t it = 0; ci.valid(); ++it, ci.next(gridDim.x)) {
-            prefetch(pi, (it + kNX - 1) % kNX);
-            pi.next(gridDim.x);
-            cp_async_wait<kNX - 1>();
-            const int as = it % kNA;
-            mbar_wait(&H->a_empty[as], ((it / kNA) & 1) ^ 1);
-            unsigned char *At = sA + as * S::kABytes;
-            const unsigned char *xt = sX + (it % kNX) * L::kXBytes;
+        // A row of item `item` (stage item % kNA) from the staged x; returns ||x|| rounded up
+        auto convert = [&](uint32_t item) -> float {
+            const TIn *xr = reinterpret_cast<const TIn *>(ring(item));
+            float x[SUB];
+            if constexpr (sizeof(TIn) == 4) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int r = p + 64 * h;
-                float x[SUB];
-                if constexpr (sizeof(TIn) == 4) {
-#pragma unroll
-                    for (int q = 0; q < SUB / 4; ++q) {
-                        const float4 v = reinterpret_cast<const float4 *>(xt + r * SUB * 4)[q];
-                        x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int tt = 0; tt < SUB; ++tt) x[tt] = (float)reinterpret_cast<const TIn *>(xt)[r * SUB + tt];
+                for (int q4 = 0; q4 < SUB / 4; ++q4) {
+                    const float4 v = reinterpret_cast<const float4 *>(xr)[q4];
+                    x[4 * q4] = v.x; x[4 * q4 + 1] = v.y; x[4 * q4 + 2] = v.z; x[4 * q4 + 3] = v.w;
                 }
-                float xh[SUB], xl[SUB], ss = 0.f;
+            } else {
 #pragma unroll
-                for (int tt = 0; tt < SUB; ++tt) {
-                    xh[tt] = tf32_rna(x[tt]);
-                    xl[tt] = tf32_rna(x[tt] - xh[tt]);
-                    ss = __fmaf_rn(x[tt], x[tt], ss);
-                }
-                unsigned char *rowp = At + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16;
+                for (int tt = 0; tt < SUB; ++tt) x[tt] = (float)xr[tt];
+            }
+            // Veltkamp split on the FMA pipe (the ALU pipe bounds the epilogue):
+            // xh = x rounded to 11 significant bits (exactly tf32), xl = x - xh exactly;
+            // the MMA reads xl truncated to tf32 (<= 2^-10 |xl| <= 2^-21 |x|).
+            float xh[SUB], xl[SUB], ss = 0.f;
+#pragma unroll
+            for (int tt = 0; tt < SUB; ++tt) {
+                const float c = __fmul_rn(x[tt], 8193.0f);
+                xh[tt] = __fsub_rn(c, __fsub_rn(c, x[tt]));
+                xl[tt] = __fsub_rn(x[tt], xh[tt]);
+                ss = __fmaf_rn(x[tt], x[tt], ss);
+            }
+            if (!(probe & 4)) {
+                unsigned char *rowp = sA + (item % kNA) * S::kABytes + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16;
                 auto st = [&](int c, float a0, float a1, float a2, float a3) {
                     *reinterpret_cast<float4 *>(rowp + c * 128) = make_float4(a0, a1, a2, a3);
                 };
@@ -352,18 +360,11 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                     st(0, xh[0], xh[1], xh[2], xh[3]); st(1, xh[0], xh[1], xh[2], xh[3]);
                     st(2, xl[0], xl[1], xl[2], xl[3]); st(3, 1.f, 1.f, 0.f, 0.f);
                 }
-                sNorm[(it % kNN) * kTM + r] = __fsqrt_ru(ss) * 1.000001f;
             }
             fence_proxy_async();
-            mbar_arrive(&H->a_full[as]);
-        }
-        cp_async_wait<0>();
-    } else {
-        // ---------------- epilogue: two groups of 4 warps, group e owns TMEM buffer e ----------------
-        const int e = (warp - 4) >> 2;
-        const int q = warp & 3;
-        const int r = 32 * q + lane;
-        constexpr float kE = (float)((3.0 / 4194304.0 + 1.0 / 131072.0 * (1.0 + 1.0 / 1024.0) + (SUB + 1) / 16777216.0) * 1.01);
+            mbar_arrive(&H->a_full[item % kNA]);
+            return __fsqrt_ru(ss) * 1.000001f;
+        };
         // b_empty[p & 1] phase p >> 1 belongs to pair p.  A group that owns no item of
         // a pair reaches the next pair early; its arrival must not land in the still
         // open phase of pair p - 2, so it first waits for that phase to complete.
@@ -371,69 +372,102 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             mbar_wait(&H->b_empty[p & 1], ((p >> 1) & 1) ^ 1);
             mbar_arrive(&H->b_empty[p & 1]);
         };
-        ItemIter ii(blockIdx.x, ngroups, ntiles, m);
-        for (uint32_t it = 0; ii.valid(); ++it, ii.next(gridDim.x)) {
+
+        ItemIter ii(blockIdx.x, ngroups, ntiles, m);   // current item
+        ItemIter ic = ii, ip = ii;                      // conversion (item + 2) / prefetch (item + 2 kPD)
+        // prologue: stage x for this group's first kPD items, convert the first one
+        uint32_t ipi = 0, ici = 0;
+        for (; ipi < (uint32_t)(2 * kPD); ++ipi, ip.next(gridDim.x))
+            if ((int)(ipi & 1) == e) prefetch(ip, ipi);
+        float norm_cur = 0.f;
+        if (ic.valid() && e == 0) { cp_async_wait<kPD - 1>(); norm_cur = convert(0); }
+        ic.next(gridDim.x); ++ici;
+        if (ic.valid() && e == 1) { cp_async_wait<kPD - 1>(); norm_cur = convert(1); }
+        ic.next(gridDim.x); ++ici;   // ic now points at item 2
+
+        for (uint32_t it = 0; ii.valid(); ++it, ii.next(gridDim.x), ic.next(gridDim.x), ip.next(gridDim.x), ++ici, ++ipi) {
             if (ii.t == 0 && it > 0) release_pair(ii.jt - 1);  // done with the previous pair's sC
             if ((int)(it & 1) != e) continue;
             const uint32_t jt = ii.jt;
             const int j = ii.j;
             mbar_wait(&H->t_full[e], (it >> 1) & 1);
+            if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 5] = clock64();
             tc_fence_after();
-            // the producer wrote this norm before a_full, which the MMA consumed before t_full
-            const float xnorm = sNorm[(it % kNN) * kTM + r];
             float bm[32], cls[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) cls[c] = pos_inf_f();
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
+            for (int ch = 0; ch < 4 && !(probe & 1); ++ch) {
                 uint32_t v[64];
                 tmem_ld64(tmem + ((uint32_t)(32 * q) << 16) + e * kN + ch * 64, v);
 #define SV(i) __uint_as_float(v[(i)])
+                if (probe & 8) {
+                    cls[ch] = __fadd_rn(SV(0), SV(63));
+                    continue;
+                }
 #pragma unroll
                 for (int bp = 0; bp < 4; ++bp) {
 #pragma unroll
                     for (int c = 0; c < 8; ++c) cls[c] = fmin3(cls[c], SV(16 * bp + c), SV(16 * bp + 8 + c));
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int o = 16 * bp + 8 * h;
-                        bm[8 * ch + 2 * bp + h] = fmin3(fmin3(SV(o), SV(o + 1), SV(o + 2)),
-                                                        fmin3(SV(o + 3), SV(o + 4), SV(o + 5)), fminf(SV(o + 6), SV(o + 7)));
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int o = 16 * bp + 8 * hh;
+                        bm[8 * ch + 2 * bp + hh] = fmin3(fmin3(SV(o), SV(o + 1), SV(o + 2)),
+                                                         fmin3(SV(o + 3), SV(o + 4), SV(o + 5)), fminf(SV(o + 6), SV(o + 7)));
                     }
                 }
 #undef SV
             }
             tc_fence_before();
             mbar_arrive(&H->t_empty[e]);
-            // blocks as a 4 (chunk) x 8 grid: winner block and second-best block
-            float G[4], Cb[8];
-#pragma unroll
-            for (int g4 = 0; g4 < 4; ++g4)
-                G[g4] = fmin3(fmin3(bm[8 * g4], bm[8 * g4 + 1], bm[8 * g4 + 2]), fmin3(bm[8 * g4 + 3], bm[8 * g4 + 4], bm[8 * g4 + 5]),
-                              fminf(bm[8 * g4 + 6], bm[8 * g4 + 7]));
-#pragma unroll
-            for (int c = 0; c < 8; ++c) Cb[c] = fminf(fmin3(bm[c], bm[8 + c], bm[16 + c]), bm[24 + c]);
-            const float m1 = fminf(fmin3(G[0], G[1], G[2]), G[3]);
-            int gs = 4, cs8 = 8, qc = 8;
-#pragma unroll
-            for (int g4 = 3; g4 >= 0; --g4) gs = (G[g4] == m1) ? g4 : gs;
-#pragma unroll
-            for (int c = 7; c >= 0; --c) { cs8 = (Cb[c] == m1) ? c : cs8; qc = (cls[c] == m1) ? c : qc; }
-            float second = pos_inf_f();
-#pragma unroll
-            for (int g4 = 0; g4 < 4; ++g4) second = (g4 == gs) ? second : fminf(second, G[g4]);
+            if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 6] = clock64();
+            // the group's next item: stage its x prefetch and write its A operand now, so
+            // its MMA can start as soon as the other group's item is done
+            if (ip.valid() || true) prefetch(ip, ipi);  // (an empty group keeps the wait count uniform)
+            float norm_next = 0.f;
+            if (ic.valid()) {
+                cp_async_wait<kPD - 1>();
+                norm_next = convert(ici);
+            }
+            const float xnorm = norm_cur;
+            norm_cur = norm_next;
+            // Final selection on the FMA pipe: ind(x) = sat(1 - (x - m1) * 2^151) is exactly 1
+            // when x == m1 and exactly 0 otherwise (also for NaN/inf), so the winner's index is
+            // sum(ind * i), the number of minima is sum(ind) (a tie -> flag), and the runner-up
+            // is min(x + ind * 3e38).  m1 comes from the class minima (every score is in one).
+            const float m1 = fmin3(fmin3(cls[0], cls[1], cls[2]), fmin3(cls[3], cls[4], cls[5]), fminf(cls[6], cls[7]));
+            float qcf = 0.f, nc = 0.f, wbf = 0.f, nb = 0.f;
+            float oc[8], ob[32];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                second = (c == cs8) ? second : fminf(second, Cb[c]);
-                second = (c == qc) ? second : fminf(second, cls[c]);
+                const float u = __fmul_rn(__fsub_rn(cls[c], m1), 8.507059e37f);  // 2^126
+                const float ind = __saturatef(__fmaf_rn(u, -33554432.0f, 1.0f)); // 2^25
+                qcf = __fmaf_rn(ind, (float)c, qcf);
+                nc = __fadd_rn(nc, ind);
+                oc[c] = __fmaf_rn(ind, 3.0e38f, cls[c]);
             }
+#pragma unroll
+            for (int b = 0; b < 32; ++b) {
+                const float u = __fmul_rn(__fsub_rn(bm[b], m1), 8.507059e37f);
+                const float ind = __saturatef(__fmaf_rn(u, -33554432.0f, 1.0f));
+                wbf = __fmaf_rn(ind, (float)b, wbf);
+                nb = __fadd_rn(nb, ind);
+                ob[b] = __fmaf_rn(ind, 3.0e38f, bm[b]);
+            }
+            float sb8[8];
+#pragma unroll
+            for (int g8 = 0; g8 < 8; ++g8) sb8[g8] = fminf(fmin3(ob[4 * g8], ob[4 * g8 + 1], ob[4 * g8 + 2]), ob[4 * g8 + 3]);
+            const float second = fmin3(fmin3(fmin3(sb8[0], sb8[1], sb8[2]), fmin3(sb8[3], sb8[4], sb8[5]), fminf(sb8[6], sb8[7])),
+                                       fmin3(oc[0], oc[1], oc[2]), fmin3(fmin3(oc[3], oc[4], oc[5]), oc[6], oc[7]));
             const float W = sGuard[2 * j] + xnorm * sGuard[2 * j + 1];
             const float thr = m1 + 4.0f * kE * W + 1e-36f;
             const int64_t row = ii.tile() * kTM + r;
-            int code = 64 * gs + 8 * cs8 + qc;
-            const bool flag = (row < n) && (!(m1 < pos_inf_f()) || !(thr < pos_inf_f()) || (gs | cs8 | qc) >= 8 ||
-                                            gs >= 4 || second <= thr);
-            // exact warp-cooperative re-encode of flagged rows (fp32 codebook from shared memory)
-            unsigned mask = __ballot_sync(0xffffffffu, flag);
+            int code = 8 * __float2int_rz(wbf) + __float2int_rz(qcf);
+            const bool flag = (row < n) && (!(m1 < pos_inf_f()) || !(thr < pos_inf_f()) || nb != 1.0f || nc != 1.0f ||
+                                            second <= thr);
+            // exact warp-cooperative re-encode of flagged rows (x and the fp32 codebook from
+            // shared memory: the item's x slot stays valid until kPD more owned items)
+            unsigned mask = __ballot_sync(0xffffffffu, flag && !(probe & 15));
             if (mask) {
                 // acquire the bulk copies of this pair (the buffer cannot advance past this
                 // pair until every epilogue thread has arrived on b_empty)
@@ -443,10 +477,11 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                 while (mask) {
                     const int src = __ffs(mask) - 1;
                     mask &= mask - 1;
-                    const int64_t srow = __shfl_sync(0xffffffffu, row, src);
+                    const TIn *xr = reinterpret_cast<const TIn *>(sX + ((size_t)e * kRing + (it >> 1) % kRing) * L::kXBytes) +
+                                    (32 * q + src) * SUB;
                     float xv[SUB];
 #pragma unroll
-                    for (int tt = 0; tt < SUB; ++tt) xv[tt] = (float)X[srow * xs + (int64_t)j * SUB + tt];
+                    for (int tt = 0; tt < SUB; ++tt) xv[tt] = (float)xr[tt];
                     float best = pos_inf_f();
                     int bl = kN;
 #pragma unroll 2
@@ -459,9 +494,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                     }
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) {
-                        const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+                        const float ob2 = __shfl_xor_sync(0xffffffffu, best, off);
                         const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
-                        if (ob < best || (ob == best && ol < bl)) { best = ob; bl = ol; }
+                        if (ob2 < best || (ob2 == best && ol < bl)) { best = ob2; bl = ol; }
                     }
                     if (lane == src) code = (best < pos_inf_f()) ? bl : 0;
                 }
@@ -470,8 +505,10 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                 codes[row * cs + j] = (uint8_t)code;
                 if (best_out) best_out[row * m + j] = m1;
             }
+            if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 7] = clock64();
         }
         if (ii.jt > 0) release_pair(ii.jt - 1);  // the last pair
+        cp_async_wait<0>();
     }
     tc_fence_before();
     __syncthreads();
@@ -527,7 +564,9 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, const float *CB, const
     const int64_t ntiles = (n + kTM - 1) / kTM;
     const int64_t ngroups = (ntiles + kG - 1) / kG;
     const int grid = (int)std::min<int64_t>(sms, ngroups);
-    kern<<<grid, kThreads, smem, st>>>(X, n, m, xs, CB, B, guard, img, codes, cs, best);
+    const char *pe = getenv("CSPQ_TC_PROBE");  // debug timing knob, see the kernel
+    const int probe = pe ? atoi(pe) : 0;
+    kern<<<grid, kThreads, smem, st>>>(X, n, m, xs, CB, B, guard, img, codes, cs, best, probe);
     CSPQ_LAUNCH_CHECK();
     return CSPQ_OK;
 }

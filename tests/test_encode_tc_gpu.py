@@ -95,7 +95,7 @@ def test_adversarial_near_ties_tensor(P, oracle):
 
 def test_tensor_error_within_band(P, oracle):
     """The guard assumes |S_tc - s_oracle| <= E = c * (max|b| + ||x|| max||c||)
-    with c ~ 8.9e-6; measure the real error on the winners and require a
+    with c ~ 2.2e-6; measure the real error on the winners and require a
     wide margin below the bound."""
     rng = np.random.default_rng(5)
     for scale in (1.0, 1e3, 1e-3):
@@ -111,4 +111,4 @@ def test_tensor_error_within_band(P, oracle):
         cmax = np.sqrt((cs.rowmajor.astype(np.float64) ** 2).sum(-1)).max(axis=1)
         W = bmax[None, :] + nrm * cmax[None, :]
         err = np.abs(best.astype(np.float64) - wbest.astype(np.float64))[same] / W[same]
-        assert err.max() < 8.9e-6 / 4, f"scale {scale}: observed {err.max():.3e} vs bound 8.9e-6"
+        assert err.max() < 2.2e-6 / 4, f"scale {scale}: observed {err.max():.3e} vs bound 2.2e-6"
