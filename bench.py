@@ -254,18 +254,40 @@ def main():
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
-            bpr = tj.get(cfg.name, {}).get("dram_bytes_per_row")
+            key = cfg.name + ("_tc" if args.mode in ("auto", "tensor") else "")
+            bpr = tj.get(key, {}).get("dram_bytes_per_row")
             traffic = None if bpr is None else int(bpr * rows)
         except Exception:
             traffic = None
+    tc = args.mode in ("auto", "tensor") and cfg.k == 256 and cfg.sub in (4, 8)
+    tf32_peak = None
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        try:
+            tf32_peak = json.load(open(mp))["bf16_tflops"] / 2.0  # dense tf32 = half of dense bf16
+        except Exception:
+            tf32_peak = None
+    if tf32_peak is None:
+        tf32_peak = 1590.0 / 2.0  # B200_PROFILING.md fallback bf16 burst / 2
+    k_eff = 32 if cfg.sub == 8 else 16  # tf32 MMA K per (row, subspace): 3xTF32 split + bias + pad
     roofline = {"bound": "fp32", "achieved": achieved, "peak": FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP32_NOMINAL_TFLOPS, "traffic": traffic,
-                "kernel": "encode_k256_kernel (guarded FFMA)" if args.mode != "exact" else "encode_k256_kernel (exact)",
-                "peak_source": "nominal FP32: 148 SMs x 128 lanes x 2 flop x 1.965 GHz (no FP32 entry in MEASURED_PEAKS.json)",
+                "kernel": ("encode_tc_kernel (tcgen05 3xTF32 + exact epilogue)" if tc else
+                           "encode_k256_kernel (" + ("exact" if args.mode == "exact" else "guarded FFMA") + ")"),
+                "peak_source": "north_star roofline = the slower of FP32 FFMA and tensor peaks: nominal FP32 "
+                               "148 SMs x 128 lanes x 2 flop x 1.965 GHz (no FP32 entry in MEASURED_PEAKS.json)",
                 "algorithmic_flops_per_row": cfg.flops_per_vec(),
                 "algorithmic_bytes_per_row": cfg.bytes_per_vec(),
                 "hbm_frac": (rows * cfg.bytes_per_vec() / (ms_per_step / 1e3) / 1e9) / 6547.8}
-
+    if tc:
+        roofline["tensor"] = {
+            "peak_tf32_tflops": tf32_peak, "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2",
+            "algorithmic_frac": achieved / tf32_peak,
+            "executed_tensor_tflops": achieved * (k_eff / cfg.sub),
+            "executed_frac": achieved * (k_eff / cfg.sub) / tf32_peak,
+            "note": f"the MMA executes K={k_eff} tf32 per (row, subspace) for {cfg.sub} useful MACs "
+                    "(hi/lo split + folded bias); the epilogue's min/max on the half-rate ALU pipe is the binding unit",
+        }
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, crow, cdt, cores = cpu_oracle_rate(cfg, dev, cs.rowmajor, cs.biases, args.cpu_seconds)

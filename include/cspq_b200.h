@@ -146,10 +146,12 @@ int cspq_encode_subspace_major(const float *P, int64_t n, int32_t m, int32_t sub
  * `device`.  Synchronous: returns when codes are in host memory.
  * batch_ms (optional, ceil(n / batch_rows) doubles) receives each batch's
  * host-observed latency from its H2D enqueue to its codes landing in host
- * memory (BASELINE config 5's per-batch p50/p99). */
+ * memory (BASELINE config 5's per-batch p50/p99).  tc_img (optional): the
+ * prepared tensor-core codebook image; when given, each batch is encoded by
+ * cspq_encode_tc instead of the FFMA kernel (same codes). */
 int cspq_encode_host(const void *X_host, int32_t in_dtype, int64_t n, int32_t d, const float *CB,
-                     const float *B, const float *guard, int32_t m, int32_t k, int32_t sub,
-                     void *codes_host, int32_t variant, int32_t mode, int64_t batch_rows,
+                     const float *B, const float *guard, const void *tc_img, int32_t m, int32_t k,
+                     int32_t sub, void *codes_host, int32_t variant, int32_t mode, int64_t batch_rows,
                      int32_t n_streams, double *batch_ms, int32_t device);
 
 /* ---------------- Lloyd k-means (training.py:57-159), all M subspaces at once.

@@ -43,7 +43,7 @@ _SIGS = {
     "cspq_encode": ([_vp, _i32, _i64, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _i32, _i32, _vp], _i32),
     "cspq_encode_with_scores": ([_vp, _i32, _i64, _i32, _i64, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _vp], _i32),
     "cspq_encode_subspace_major": ([_vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _i32, _vp], _i32),
-    "cspq_encode_host": ([_vp, _i32, _i64, _i32, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _i32, _i32, _i64, _i32, _vp, _i32], _i32),
+    "cspq_encode_host": ([_vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _i32, _i32, _i64, _i32, _vp, _i32], _i32),
     "cspq_lloyd_workspace_bytes": ([_i64, _i32, _i32, _i32], ctypes.c_size_t),
     "cspq_lloyd_assign": ([_vp, _i32, _i64, _i32, _i32, _i32, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp], _i32),
     "cspq_lloyd_accumulate": ([_vp, _i32, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp], _i32),

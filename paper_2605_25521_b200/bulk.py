@@ -265,8 +265,14 @@ def encode_dataset_host(X: np.ndarray, codebooks, plan: ExecutionPlan | None = N
     nb = -(-n // plan.resolved_batch_rows())
     if batch_ms is not None and batch_ms.shape[0] < nb:
         raise ConfigError("batch_ms too small")
+    img = None
+    if plan.mode in ("auto", "tensor") and vid != N.VARIANT_REFERENCE and cbset.k == 256 and cbset.sub_dim in (4, 8):
+        img = cbset.tc_image(dev, nobias=not precomputed_bias and plan.variant is EncoderVariant.BLOCKED)
+    elif plan.mode == "tensor":
+        raise ConfigError("mode='tensor' needs k=256, sub_dim in {4, 8} and a REFORMULATED/BLOCKED variant")
+    t.cuda.current_stream(dev).synchronize()  # image preparation visible to the pipeline streams
     N.call("cspq_encode_host", X.ctypes.data_as(ctypes.c_void_p), N.IN_U8 if in_u8 else N.IN_F32, n, d,
-           ptr(rm), ptr(bs), ptr(guard), cbset.m, cbset.k, cbset.sub_dim,
+           ptr(rm), ptr(bs), ptr(guard), ptr(img), cbset.m, cbset.k, cbset.sub_dim,
            out.ctypes.data_as(ctypes.c_void_p), vid, _MODES[plan.mode], plan.resolved_batch_rows(),
            plan.streams, None if batch_ms is None else batch_ms.ctypes.data_as(ctypes.c_void_p),
            dev.index)

@@ -251,8 +251,9 @@ int cspq_encode_subspace_major(const float *P, int64_t n, int32_t m, int32_t sub
 }
 
 int cspq_encode_host(const void *X_host, int32_t in_dtype, int64_t n, int32_t d, const float *CB, const float *B,
-                     const float *guard, int32_t m, int32_t k, int32_t sub, void *codes_host, int32_t variant,
-                     int32_t mode, int64_t batch_rows, int32_t n_streams, double *batch_ms, int32_t device) {
+                     const float *guard, const void *tc_img, int32_t m, int32_t k, int32_t sub, void *codes_host,
+                     int32_t variant, int32_t mode, int64_t batch_rows, int32_t n_streams, double *batch_ms,
+                     int32_t device) {
     int rc = check_shape(n, m, k, sub);
     if (rc) return rc;
     CSPQ_REQUIRE(d == m * sub, CSPQ_E_CONFIG,
@@ -307,8 +308,12 @@ int cspq_encode_host(const void *X_host, int32_t in_dtype, int64_t n, int32_t d,
         cudaStream_t st = P.st[s];
         CSPQ_CUDA_TRY(cudaEventRecord(P.ev0[s], st));
         CSPQ_CUDA_TRY(cudaMemcpyAsync(P.dX[s], src, rows * xrow, cudaMemcpyHostToDevice, st));
-        if ((rc = encode_device(P.dX[s], in_dtype, rows, d, d, CB, B, guard, m, k, sub, P.dC[s], m, variant, mode, st)))
-            return rc;
+        if (tc_img && variant != CSPQ_VARIANT_REFERENCE)
+            rc = encode_tc(P.dX[s], in_dtype, rows, d, CB, B, guard, tc_img, m, k, sub,
+                           reinterpret_cast<uint8_t *>(P.dC[s]), m, nullptr, st);
+        else
+            rc = encode_device(P.dX[s], in_dtype, rows, d, d, CB, B, guard, m, k, sub, P.dC[s], m, variant, mode, st);
+        if (rc) return rc;
         void *dst = pin_out ? (char *)codes_host + r0 * crow : P.hC[s];
         CSPQ_CUDA_TRY(cudaMemcpyAsync(dst, P.dC[s], rows * crow, cudaMemcpyDeviceToHost, st));
         CSPQ_CUDA_TRY(cudaEventRecord(P.ev1[s], st));
