@@ -186,3 +186,26 @@ def test_config_training_vs_oracle(P, oracle, name):
         assert res[j].iterations == o["iterations"]
         assert res[j].centroids.tobytes() == o["centroids"].tobytes(), (name, j)
         assert res[j].objectives == o["objectives"]
+
+
+def test_sharded_driver_matches_batched_lloyd(P):
+    """distributed.lloyd_sharded on the CUDA step backend (world size 1, both
+    reduce modes) reproduces cspq_lloyd_train bit for bit."""
+    import torch
+    from paper_2605_25521_b200.distributed import CudaSteps, lloyd_sharded
+    rng = np.random.default_rng(12)
+    m, n, sub, k = 3, 4000, 8, 64
+    pts = rng.standard_normal((m, n, sub)).astype(np.float32)
+    init = pts[:, :k].astype(np.float64).copy()
+    init[:, 5] = init[:, 4]
+    cfg = P.TrainConfig(k=k, max_iters=12, tol=1e-5)
+    ref = P.lloyd_iterate_batched(pts, init, cfg)
+    dev = torch.device("cuda", 0)
+    Pd = torch.from_numpy(pts).to(dev)
+    for mode in ("allgather", "allreduce"):
+        res = lloyd_sharded(CudaSteps(Pd, 0, n, m, sub, k, dev), torch.from_numpy(init).to(dev), cfg, reduce=mode)
+        for a, b in zip(res, ref):
+            assert a.iterations == b.iterations
+            assert a.centroids.tobytes() == b.centroids.tobytes()
+            assert a.objectives == b.objectives
+            assert np.array_equal(a.assignments, b.assignments)
