@@ -84,13 +84,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                  "r"(bytes) : "memory");
 }
 // bounded wait: a lost arrival traps (error) instead of hanging the device
+constexpr uint32_t kSuspendNs = 1000000;
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
     for (uint64_t spin = 0;; ++spin) {
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        // suspend (woken by the phase flip) instead of busy polling: spinning warps steal
+        // issue slots from the epilogue warps that share their SM sub-partition
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity), "r"(kSuspendNs) : "memory");
         if (done) return;
-        if (spin > (1ull << 31)) __trap();
+        if (spin > (1ull << 26)) __trap();  // seconds of waiting: a hang
     }
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -206,7 +209,8 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                  uint8_t *__restrict__ codes, int64_t cs, float *__restrict__ best_out, int probe) {
     // probe (debug timing only): bit 0 = epilogue skips its min work, bit 1 = no MMAs,
     // bit 2 = skip the A conversion, bit 3 = keep TMEM loads but skip the min work
-    // (bits 0-3 leave garbage codes), bit 4 = CTA 0 writes clock64 stamps into best_out
+    // (bits 0-3 leave garbage codes), bit 4 = CTA 0 writes clock64 stamps into best_out,
+    // bit 5 = no x prefetch (stale x), bit 6 = no code stores
     using S = TcShape<SUB>;
     using L = TcSmem<SUB, TIn>;
     long long *stamp = (probe & 16) && blockIdx.x == 0 ? reinterpret_cast<long long *>(best_out) : nullptr;
@@ -423,10 +427,10 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 6] = clock64();
             // the group's next item: stage its x prefetch and write its A operand now, so
             // its MMA can start as soon as the other group's item is done
-            if (ip.valid() || true) prefetch(ip, ipi);  // (an empty group keeps the wait count uniform)
+            if (!(probe & 32)) prefetch(ip, ipi);  // (an empty group keeps the wait count uniform)
             float norm_next = 0.f;
             if (ic.valid()) {
-                cp_async_wait<kPD - 1>();
+                if (!(probe & 32)) cp_async_wait<kPD - 1>();
                 norm_next = convert(ici);
             }
             const float xnorm = norm_cur;
@@ -502,7 +506,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                 }
             }
             if (row < n) {
-                codes[row * cs + j] = (uint8_t)code;
+                if (!(probe & 64)) codes[row * cs + j] = (uint8_t)code;
                 if (best_out) best_out[row * m + j] = m1;
             }
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 7] = clock64();

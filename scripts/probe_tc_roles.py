@@ -21,7 +21,7 @@ for _ in range(3): P.encode_dataset_device(X, cs, plan, out=out)
 e1.record(); torch.cuda.synchronize()
 print(os.environ.get("CSPQ_TC_PROBE", "0"), e0.elapsed_time(e1) / 3, "ms")
 '''
-for pr in ["0", "8", "1", "4", "12", "2"]:
+for pr in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["0", "8", "1", "4", "12", "2"]):
     env = dict(os.environ, CSPQ_TC_PROBE=pr)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     print(r.stdout.strip(), r.stderr.strip()[-200:] if r.returncode else "", flush=True)
