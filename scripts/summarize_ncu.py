@@ -67,9 +67,10 @@ def full(path, out, rows=None):
         k["stall_share"] = {a: round(b / tot, 4) for a, b in sorted(st.items(), key=lambda kv: -kv[1])[:10]}
         if rows:
             try:
-                byt = float(d["dram__bytes_read.sum"].replace(",", "")) + float(d["dram__bytes_write.sum"].replace(",", ""))
-                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u["dram__bytes_read.sum"], 1)
-                k["dram_bytes_per_row"] = byt * scale / rows
+                sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+                byt = sum(float(d[key].replace(",", "")) * sc.get(u[key], 1)  # each metric has its own unit
+                          for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+                k["dram_bytes_per_row"] = byt / rows
             except Exception:
                 pass
         res["kernels"].append(k)
