@@ -41,7 +41,8 @@ def parse():
     p.add_argument("--rows", type=int, default=0, help="rows per rank (0 = the config's N)")
     p.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     p.add_argument("--mode", default="auto", choices=["auto", "exact", "guarded"])
-    p.add_argument("--e2e-rows", type=int, default=2_000_000)
+    p.add_argument("--e2e-rows", type=int, default=0,
+                   help="rows per rank through the host API (0 = 2M, or the whole config for c5)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -195,24 +196,34 @@ def main():
         parity = {"rows_checked": int(idx.shape[0]), "code_mismatches": int((got != want).sum())}
 
     # ---- device-resident timed region ----
+    # inputs smaller than 2x L2 (c1: 51 MB) would be served from the 126 MB L2 on repeat
+    # steps: flush it with an untimed 4x-L2 write between steps and time each step alone
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    in_bytes = rows * cfg.d * cfg.elem_bytes
+    flush = torch.empty(4 * l2, dtype=torch.uint8, device=dev) if in_bytes < 2 * l2 else None
     for _ in range(args.warmup):
         P.encode_dataset_device(X, cs, plan, out=out)
     N.call("cspq_encode_stats", None, 1)
     clocks = ClockSampler(local).start()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev[0].record(stream)
     for s in range(args.steps):
+        if flush is not None:
+            flush.fill_(s & 0xff)
+        ev[2 * s].record(stream)
         P.encode_dataset_device(X, cs, plan, out=out)
-        ev[s + 1].record(stream)
+        ev[2 * s + 1].record(stream)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     clk = clocks.stop()
-    step_ms = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
-    total_ms = ev[0].elapsed_time(ev[-1])
+    step_ms = [ev[2 * s].elapsed_time(ev[2 * s + 1]) for s in range(args.steps)]
+    total_ms = sum(step_ms) if flush is not None else ev[0].elapsed_time(ev[-1])
+    l2_note = (f"L2 flushed between steps (untimed {4 * l2 >> 20} MB write; input {in_bytes / 2**20:.0f} MB < 2x L2)"
+               if flush is not None else f"inputs larger than L2 ({in_bytes / 1e9:.1f} GB/GPU)")
+    del flush
     fl = ctypes.c_uint64(0)
     N.call("cspq_encode_stats", ctypes.byref(fl), 1)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -225,25 +236,37 @@ def main():
     # ---- end-to-end through the public API with pinned host buffers ----
     e2e = None
     if not args.no_e2e:
-        ne = min(args.e2e_rows, rows)
+        # c5 is the streaming config: the reference's 4096-row batches from pinned host memory,
+        # whole dataset per step, with per-batch H2D -> encode -> D2H latency from device events
+        ne = min(args.e2e_rows or (cfg.n if cfg.batch else 2_000_000), rows)
+        batch_rows = cfg.batch or (1 << 18)
         Xh = P.pinned_empty((ne, cfg.d), np.uint8 if cfg.dtype == "u8" else np.float32)
         Xh[:] = X[:ne].cpu().numpy()
         codes_h = P.pinned_empty((ne, cfg.m), np.uint8)
-        eplan = P.ExecutionPlan(mode=args.mode, batch_rows=1 << 18, streams=3)
+        eplan = P.ExecutionPlan(mode=args.mode, batch_rows=batch_rows, streams=3)
+        nb = (ne + batch_rows - 1) // batch_rows
+        bms = np.zeros(nb, np.float64)
         P.encode_dataset_host(Xh, cs, eplan, out=codes_h)  # warm the pipeline
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        lat = []
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            P.encode_dataset_host(Xh, cs, eplan, out=codes_h)
+            P.encode_dataset_host(Xh, cs, eplan, out=codes_h, batch_ms=bms)
+            lat.append(bms.copy())
         el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if ws > 1:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
         e2e_val = ne * ws * args.steps / float(el.item())
         assert np.array_equal(codes_h[:4096], out[:4096].cpu().numpy()), "e2e codes differ from device codes"
+        lat = np.concatenate(lat)
         e2e = {"value": e2e_val, "unit": "vectors/s", "h2d_bytes_per_step": int(ne * cfg.d * cfg.elem_bytes) * ws,
-               "d2h_bytes_per_step": int(ne * cfg.m) * ws, "rows_per_gpu": ne,
+               "d2h_bytes_per_step": int(ne * cfg.m) * ws, "rows_per_gpu": ne, "batch_rows": batch_rows,
+               "batch_latency_ms": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
+                                    "batches": int(lat.shape[0]),
+                                    "def": "device events: H2D start -> D2H end of one batch (3 batches in flight)"},
+               "h2d_GBps": ne * cfg.d * cfg.elem_bytes * args.steps / float(el.item()) / 1e9,
                "path": "encode_dataset_host (pinned numpy -> cspq_encode_host: 3-stream H2D/encode/D2H pipeline)"}
 
     # ---- roofline of the encode kernel ----
@@ -288,6 +311,27 @@ def main():
             "note": f"the MMA executes K={k_eff} tf32 per (row, subspace) for {cfg.sub} useful MACs "
                     "(hi/lo split + folded bias); the epilogue's min/max on the half-rate ALU pipe is the binding unit",
         }
+    # ---- c2's timed scope is train + encode: report the GPU Lloyd beside the encode ----
+    train = None
+    if rank == 0 and cfg.codebook == "lloyd" and cfg.name == "c2":
+        enc_s = ms_per_step / 1e3
+        train = {"gpu_s": train_s, "subspaces": cfg.m, "iters": cfg.iters, "sample_rows": cfg.n_train,
+                 "train_plus_encode_vec_s": rows / (train_s + enc_s),
+                 "def": "wall time of one lloyd_iterate_batched call (all subspaces, fp64, tol=0) incl. the final "
+                        "REFERENCE pass and host transfer of the results"}
+        if ws == 1 and not args.no_cpu_baseline:
+            from oracle import oracle as O
+            S = C.training_sample(cfg, dev)
+            Ssm = C.subspace_major(S, cfg.m)
+            init = C.lloyd_init(cfg, Ssm)
+            p0 = Ssm[0].double().cpu().numpy()
+            t0 = time.perf_counter()
+            O.lloyd(p0, init[0], cfg.iters, 0.0)
+            one = time.perf_counter() - t0
+            train["cpu_baseline"] = {"seconds": one * cfg.m, "kind": "port", "cores": os.cpu_count() or 1,
+                                     "sample": f"oracle.lloyd on subspace 0 ({cfg.n_train:,} x {cfg.sub} fp64, "
+                                               f"{cfg.iters} iters) in {one:.2f} s, x {cfg.m} subspaces"}
+            del S, Ssm
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, crow, cdt, cores = cpu_oracle_rate(cfg, dev, cs.rowmajor, cs.biases, args.cpu_seconds)
@@ -302,12 +346,13 @@ def main():
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_desc(cfg, rows, ws, args.scaling), "global_batch": rows * ws,
                        "rows_per_gpu": rows, "parallelism": f"rows sharded x{ws} (codebooks NCCL-broadcast)",
-                       "mode": args.mode, "codebook_train_s": train_s, "l2": "inputs larger than L2 (30.7 GB/GPU)" if cfg.name == "c3"
-                       else "inputs larger than L2"},
+                       "mode": args.mode, "codebook_train_s": train_s, "l2": l2_note},
             "clocks": clk, "e2e": e2e, "gpu_launches": args.steps, "roofline": roofline, "cpu_baseline": cpu,
             "parity": parity, "flagged_per_subvector": fl.value / max(1, rows * cfg.m * args.steps),
             "step_ms": step_ms,
         }
+        if train is not None:
+            line["train"] = train
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
