@@ -51,6 +51,7 @@ extern "C" {
 #define CSPQ_E_CUDA (-3)     /* CUDA runtime failure                          */
 #define CSPQ_E_NOMEM (-4)    /* allocation failure                            */
 #define CSPQ_E_TRAINING (-5) /* cannot train            -> cspq TrainingError */
+#define CSPQ_E_FORMAT (-6)   /* malformed file          -> cspq FormatError   */
 
 /* input element type of X */
 #define CSPQ_IN_F32 0
@@ -237,6 +238,53 @@ int cspq_lloyd_final_objective(const void *P, int32_t p_f64, int64_t n, int32_t 
 int cspq_kmeanspp(const void *P, int32_t p_f64, int64_t n, int32_t m, int32_t sub, int32_t k,
                   const int64_t *first, const double *u, double *C64, int32_t *status,
                   void *workspace, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Data formats either side of the path (io.py).  CRC-32 is zlib's, the
+ * trailer of the PQCB / PQCD containers (io.py:140-151, 213-219).
+ * ------------------------------------------------------------------------- */
+
+/* Scratch bytes cspq_crc32_device needs for n input bytes. */
+size_t cspq_crc32_workspace_bytes(int64_t n);
+
+/* *crc_out (device uint32) = zlib.crc32(data[0:n], crc_in) for n device
+ * bytes: per-thread pieces merged in GF(2) (crc(A|B) = x^(8|B|) crc(A) ^
+ * crc(B)).  Replaces the host zlib.crc32 pass of write_codes (io.py:213-219)
+ * for codes that live on the GPU. */
+int cspq_crc32_device(const void *data, int64_t n, uint32_t crc_in, uint32_t *crc_out,
+                      void *workspace, void *stream);
+
+/* Host helper: the CRC of A || B from crc(A), crc(B) and |B| (zlib's
+ * crc32_combine). */
+uint32_t cspq_crc32_combine(uint32_t crc_a, uint32_t crc_b, int64_t len_b);
+
+/* texmex records (fvecs: value_bytes 4, bvecs: 1; io.py:35-62, 100-104) ->
+ * dense (n, d) rows, validating on the device: bad[0] (uint64, init
+ * ~0) = min file offset of a record header != d, bad[1] = min file offset
+ * of a non-finite value (check_finite, io.py:70-77); offset0 = file offset
+ * of the first record. */
+int cspq_unpack_vecs(const void *records, int64_t n, int32_t d, int32_t value_bytes,
+                     int32_t check_finite, int64_t offset0, void *rows, uint64_t *bad,
+                     void *stream);
+
+/* Streaming file encoder: fvecs (in_format 0) or bvecs (1) file -> PQCD
+ * codes file (io.py:213-219), i.e. read_fvecs/read_bvecs + encode_dataset +
+ * write_codes (bulk.py:108-157) without materialising the dataset: batches
+ * of batch_rows records are pread into pinned buffers, copied raw to the
+ * GPU, unpacked and validated there, encoded (tc_img != NULL: tcgen05 path),
+ * checksummed on the GPU and written with pwrite, n_streams batches in
+ * flight.  bvecs rows are encoded as uint8 (no float32 widening copy).
+ * On a format problem returns CSPQ_E_FORMAT, removes out_path and sets
+ * err[0] = kind (1 empty dataset, 2 truncated record header, 3 non-positive
+ * record length, 4 inconsistent record length, 5 truncated record body,
+ * 6 non-finite value), err[1] = byte offset, err[2] = the offending record
+ * length (kinds 3, 4) -- the reference reader's checks and precedence
+ * (io.py:35-77).  *n_rows = records encoded.  Synchronous. */
+int cspq_encode_vecs_file(const char *in_path, int32_t in_format, const char *out_path,
+                          const float *CB, const float *B, const float *guard, const void *tc_img,
+                          int32_t m, int32_t k, int32_t sub, int32_t variant, int32_t mode,
+                          int64_t batch_rows, int32_t n_streams, int32_t device, int64_t *n_rows,
+                          int64_t *err);
 
 #ifdef __cplusplus
 }

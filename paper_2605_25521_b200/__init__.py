@@ -56,12 +56,29 @@ from .bulk import (
     encode_dataset_host,
     estimate_working_set,
 )
+from .io import (
+    crc32_device,
+    encode_file,
+    read_bvecs,
+    read_codebooks,
+    read_codes,
+    read_fvecs,
+    read_ivecs,
+    synth_dataset,
+    write_bvecs,
+    write_codebooks,
+    write_codes,
+    write_fvecs,
+    write_ivecs,
+)
 from ._device import pinned_empty
 from ._native import NativeUnavailable
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "crc32_device", "encode_file", "read_bvecs", "read_codebooks", "read_codes", "read_fvecs", "read_ivecs",
+    "synth_dataset", "write_bvecs", "write_codebooks", "write_codes", "write_fvecs", "write_ivecs",
     "CHUNK_MAJOR", "VECTOR_MAJOR", "Codebook", "CodebookSet", "ConfigError", "CorruptionError",
     "DataError", "EncoderVariant", "Error", "ExecutionPlan", "FormatError", "KMeansResult",
     "NativeUnavailable", "PQCodes", "PQParams", "ScoreBlock", "TrainConfig", "TrainingError",

@@ -24,6 +24,7 @@ CSPQ_E_DATA = -2
 CSPQ_E_CUDA = -3
 CSPQ_E_NOMEM = -4
 CSPQ_E_TRAINING = -5
+CSPQ_E_FORMAT = -6
 
 IN_F32, IN_U8 = 0, 1
 VARIANT_REFERENCE, VARIANT_REFORMULATED, VARIANT_BLOCKED = 0, 1, 2
@@ -53,6 +54,12 @@ _SIGS = {
     "cspq_lloyd_train": ([_vp, _i32, _i64, _i32, _i32, _i32, _vp, _i32, _dbl, _vp, _vp, _vp, _vp, _vp, _vp], _i32),
     "cspq_lloyd_final_objective": ([_vp, _i32, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp], _i32),
     "cspq_kmeanspp": ([_vp, _i32, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp], _i32),
+    "cspq_crc32_workspace_bytes": ([_i64], ctypes.c_size_t),
+    "cspq_crc32_device": ([_vp, _i64, ctypes.c_uint32, _vp, _vp, _vp], _i32),
+    "cspq_crc32_combine": ([ctypes.c_uint32, ctypes.c_uint32, _i64], ctypes.c_uint32),
+    "cspq_unpack_vecs": ([_vp, _i64, _i32, _i32, _i32, _i64, _vp, _vp, _vp], _i32),
+    "cspq_encode_vecs_file": ([ctypes.c_char_p, _i32, ctypes.c_char_p, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
+                               _i32, _i64, _i32, _i32, _vp, _vp], _i32),
 }
 
 _lib = None
@@ -105,11 +112,15 @@ def header_symbols() -> list[str]:
 
 def call(name: str, *args):
     """Call an entry point and map its status to the package's exceptions."""
-    from .core import ConfigError, DataError, TrainingError
-    fn = getattr(load(), name)
-    rc = fn(*args)
-    if rc == CSPQ_OK:
-        return rc
+    rc = getattr(load(), name)(*args)
+    if rc != CSPQ_OK:
+        raise_status(rc, name)
+    return rc
+
+
+def raise_status(rc: int, name: str):
+    """Raise the package exception for a non-zero CSPQ_E* status."""
+    from .core import ConfigError, DataError, FormatError, TrainingError
     msg = load().cspq_last_error().decode(errors="replace")
     if rc == CSPQ_E_CONFIG:
         raise ConfigError(msg)
@@ -117,6 +128,8 @@ def call(name: str, *args):
         raise DataError(msg)
     if rc == CSPQ_E_TRAINING:
         raise TrainingError(msg)
+    if rc == CSPQ_E_FORMAT:
+        raise FormatError(msg)
     raise RuntimeError(f"{name} failed ({rc}): {msg}")
 
 

@@ -32,6 +32,14 @@ int encode_subspace_major(const float *P, int64_t n, int m, int sub, const float
 int encode_with_scores(const void *X, int in_dtype, int64_t n, int64_t xrs, const float *CB, const float *B,
                        int m, int k, int sub, int32_t *codes, float *best, int variant, cudaStream_t st);
 size_t lloyd_workspace_bytes(int64_t n, int m, int sub, int k);
+size_t crc32_workspace_bytes(int64_t n);
+int crc32_device_api(const void *data, int64_t n, uint32_t crc_in, uint32_t *crc_out, void *ws, cudaStream_t st);
+uint32_t crc32_combine_host(uint32_t crc1, uint32_t crc2, int64_t len2);
+int unpack_vecs(const void *records, int64_t n, int d, int value_bytes, int check_finite, int64_t off0, void *rows,
+                unsigned long long *bad, cudaStream_t st);
+int encode_vecs_file(const char *in_path, int fmt, const char *out_path, const float *CB, const float *B,
+                     const float *guard, const void *tc_img, int m, int k, int sub, int variant, int mode,
+                     int64_t batch_rows, int n_streams, int device, int64_t *n_out, int64_t *err);
 int lloyd_assign(const void *P, int pf64, int64_t n, int m, int sub, int k, const double *C64,
                  const int32_t *state, int64_t b, int64_t e, int32_t *assign, double *sq, void *ws, cudaStream_t st);
 int lloyd_accumulate(const void *P, int pf64, int64_t n, int m, int sub, int k, const int32_t *state,
@@ -322,6 +330,45 @@ int cspq_encode_host(const void *X_host, int32_t in_dtype, int64_t n, int32_t d,
     for (int s = 0; s < n_streams; ++s)
         if ((rc = retire(s))) return rc;
     return CSPQ_OK;
+}
+
+size_t cspq_crc32_workspace_bytes(int64_t n) { return crc32_workspace_bytes(n); }
+
+int cspq_crc32_device(const void *data, int64_t n, uint32_t crc_in, uint32_t *crc_out, void *workspace,
+                      void *stream) {
+    CSPQ_REQUIRE(n >= 0, CSPQ_E_CONFIG, "n must be >= 0");
+    CSPQ_REQUIRE(crc_out && workspace && (data || n == 0), CSPQ_E_CONFIG, "null pointer");
+    return crc32_device_api(data, n, crc_in, crc_out, workspace, as_stream(stream));
+}
+
+uint32_t cspq_crc32_combine(uint32_t crc_a, uint32_t crc_b, int64_t len_b) {
+    return crc32_combine_host(crc_a, crc_b, len_b);
+}
+
+int cspq_unpack_vecs(const void *records, int64_t n, int32_t d, int32_t value_bytes, int32_t check_finite,
+                     int64_t offset0, void *rows, uint64_t *bad, void *stream) {
+    CSPQ_REQUIRE(n >= 0 && d >= 1, CSPQ_E_CONFIG, "bad shape");
+    CSPQ_REQUIRE(value_bytes == 1 || value_bytes == 4, CSPQ_E_CONFIG, "value_bytes must be 1 or 4");
+    if (n == 0) return CSPQ_OK;
+    CSPQ_REQUIRE(records && rows && bad, CSPQ_E_CONFIG, "null pointer");
+    return unpack_vecs(records, n, d, value_bytes, check_finite, offset0, rows,
+                       reinterpret_cast<unsigned long long *>(bad), as_stream(stream));
+}
+
+int cspq_encode_vecs_file(const char *in_path, int32_t in_format, const char *out_path, const float *CB,
+                          const float *B, const float *guard, const void *tc_img, int32_t m, int32_t k, int32_t sub,
+                          int32_t variant, int32_t mode, int64_t batch_rows, int32_t n_streams, int32_t device,
+                          int64_t *n_rows, int64_t *err) {
+    int rc = check_shape(0, m, k, sub);
+    if (rc) return rc;
+    CSPQ_REQUIRE(in_path && out_path && n_rows && err && CB, CSPQ_E_CONFIG, "null pointer");
+    CSPQ_REQUIRE(in_format == 0 || in_format == 1, CSPQ_E_CONFIG, "in_format must be 0 (fvecs) or 1 (bvecs)");
+    CSPQ_REQUIRE(variant >= 0 && variant <= 2 && mode >= 0 && mode <= 2, CSPQ_E_CONFIG, "bad variant/mode");
+    CSPQ_REQUIRE(B || variant == CSPQ_VARIANT_REFERENCE, CSPQ_E_CONFIG, "null biases");
+    CSPQ_REQUIRE(batch_rows >= 1 && n_streams >= 1 && n_streams <= 8, CSPQ_E_CONFIG, "bad pipeline shape");
+    CSPQ_REQUIRE(device >= 0 && device < 64, CSPQ_E_CONFIG, "bad device %d", device);
+    return encode_vecs_file(in_path, in_format, out_path, CB, B, guard, tc_img, m, k, sub, variant, mode, batch_rows,
+                            n_streams, device, n_rows, err);
 }
 
 size_t cspq_lloyd_workspace_bytes(int64_t n, int32_t m, int32_t sub, int32_t k) {

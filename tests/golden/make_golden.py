@@ -210,12 +210,91 @@ def pairwise_cases():
     return out
 
 
+def io_cases():
+    """File bytes written by the reference's own writers (io.py) and the
+    errors its readers raise, for the format layer and the GPU file encoder."""
+    import struct
+    import tempfile
+    from cspq import bulk, core, io
+    out = {}
+    rng = np.random.default_rng(20260202)
+    tmp = tempfile.mkdtemp()
+
+    def raw(name, path):
+        out[name] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8).copy()
+
+    # vector files
+    f32 = rng.standard_normal((37, 24)).astype(np.float32)
+    u8 = rng.integers(0, 256, (29, 16)).astype(np.uint8)
+    i32 = rng.integers(0, 5000, (11, 7)).astype(np.int32)
+    io.write_fvecs(os.path.join(tmp, "a.fvecs"), f32)
+    io.write_bvecs(os.path.join(tmp, "a.bvecs"), u8)
+    io.write_ivecs(os.path.join(tmp, "a.ivecs"), i32)
+    out["fvecs/data"], out["bvecs/data"], out["ivecs/data"] = f32, u8, i32
+    for ext in ("fvecs", "bvecs", "ivecs"):
+        raw(f"{ext}/bytes", os.path.join(tmp, f"a.{ext}"))
+    # containers
+    cbs = [core.Codebook.from_rowmajor(j, rng.standard_normal((16, 4)).astype(np.float32)) for j in range(3)]
+    io.write_codebooks(os.path.join(tmp, "c.pqcb"), cbs)
+    raw("pqcb/bytes", os.path.join(tmp, "c.pqcb"))
+    out["pqcb/rowmajor"] = np.stack([c.centroids_rowmajor for c in cbs])
+    c8 = core.PQCodes(codes=rng.integers(0, 200, (50, 4)).astype(np.uint8), k=200)
+    c16 = core.PQCodes(codes=rng.integers(0, 1000, (20, 3)).astype(np.uint16), k=1000)
+    io.write_codes(os.path.join(tmp, "c8.pqcd"), c8)
+    io.write_codes(os.path.join(tmp, "c16.pqcd"), c16)
+    raw("pqcd8/bytes", os.path.join(tmp, "c8.pqcd"))
+    raw("pqcd16/bytes", os.path.join(tmp, "c16.pqcd"))
+    out["pqcd8/codes"], out["pqcd16/codes"] = c8.codes, c16.codes
+    # encode-from-file cases: read_fvecs / read_bvecs + encode_dataset + write_codes
+    for name, ext, X, sub in (("file_f32", "fvecs", (rng.standard_normal((3000, 64)) * 3).astype(np.float32), 8),
+                              ("file_u8", "bvecs", rng.integers(0, 256, (2500, 32)).astype(np.uint8), 4)):
+        m = X.shape[1] // sub
+        Xf = X.astype(np.float32)
+        rm = np.stack([Xf[rng.choice(X.shape[0], 256, replace=False), j * sub:(j + 1) * sub] for j in range(m)])
+        rm = rm + rng.normal(0, 0.25, rm.shape).astype(np.float32)
+        cset = bulk.CodebookSet.from_codebooks([core.Codebook.from_rowmajor(j, rm[j]) for j in range(m)])
+        path = os.path.join(tmp, f"{name}.{ext}")
+        (io.write_fvecs if ext == "fvecs" else io.write_bvecs)(path, X)
+        ds = (io.read_fvecs if ext == "fvecs" else io.read_bvecs)(path)
+        codes = bulk.encode_dataset(ds, cset)
+        io.write_codes(os.path.join(tmp, f"{name}.pqcd"), codes)
+        out[f"{name}/X"], out[f"{name}/rowmajor"] = X, cset.rowmajor
+        raw(f"{name}/vecs_bytes", path)
+        raw(f"{name}/pqcd_bytes", os.path.join(tmp, f"{name}.pqcd"))
+    # reader errors: (message, offset) for malformed files
+    bad = {
+        "empty": b"",
+        "inconsistent": struct.pack("<i", 2) + struct.pack("<2f", 1, 2) + struct.pack("<i", 3) + struct.pack("<3f", 1, 2, 3),
+        "truncated_body": struct.pack("<i", 4) + struct.pack("<2f", 1, 2),
+        "truncated_header": struct.pack("<i", 2) + struct.pack("<2f", 1, 2) + b"\x02\x00",
+        "nonpositive": struct.pack("<i", 2) + struct.pack("<2f", 1, 2) + struct.pack("<i", -1),
+        "nonfinite": struct.pack("<i", 2) + struct.pack("<2f", 1, 2) + struct.pack("<i", 2) + struct.pack("<2f", 3, float("inf")),
+    }
+    msgs = []
+    for key, b in bad.items():
+        path = os.path.join(tmp, f"{key}.fvecs")
+        open(path, "wb").write(b)
+        try:
+            io.read_fvecs(path)
+            msgs.append((key, "", -1))
+        except core.FormatError as e:
+            msgs.append((key, str(e).replace(path, "<path>"), -1 if e.offset is None else e.offset))
+        out[f"err/{key}/bytes"] = np.frombuffer(b, dtype=np.uint8).copy()
+    out["err/keys"] = np.array([k for k, _, _ in msgs])
+    out["err/messages"] = np.array([msg for _, msg, _ in msgs])
+    out["err/offsets"] = np.array([o for _, _, o in msgs], dtype=np.int64)
+    # synth_dataset bits
+    out["synth/data"] = io.synth_dataset(64, 12, 5, seed=7).data
+    return out
+
+
 def main():
     bulk, core, kernels, training = _ref()
     np.savez_compressed(os.path.join(HERE, "encode_golden.npz"), **encode_cases(bulk, core, kernels))
     np.savez_compressed(os.path.join(HERE, "lloyd_golden.npz"), **lloyd_cases(training))
     np.savez_compressed(os.path.join(HERE, "train_golden.npz"), **train_cases(core, training))
     np.savez_compressed(os.path.join(HERE, "pairwise_golden.npz"), **pairwise_cases())
+    np.savez_compressed(os.path.join(HERE, "io_golden.npz"), **io_cases())
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
