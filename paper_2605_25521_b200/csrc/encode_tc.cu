@@ -55,10 +55,11 @@ namespace {
 constexpr int kTM = 128;     // rows per tile (MMA M)
 constexpr int kN = 256;      // centroids (MMA N)
 constexpr int kG = 8;        // tiles per row group (codebook image reuse)
-constexpr int kNA = 4;       // A-operand stages
-constexpr int kThreads = 320;  // 10 warps: MMA, loader, 2 x 4 epilogue/producer
-constexpr int kPD = 3;        // cp.async prefetch distance, in the group's own items
-constexpr int kRing = 4;      // x slots per group (> kPD: an item's slot outlives its fix-up)
+constexpr int kGroups = 3;   // epilogue groups: item it belongs to group it % kGroups
+constexpr int kNA = kGroups; // A-operand stages (a group writes item it + kGroups into item it's stage)
+constexpr int kThreads = 64 + 128 * kGroups;  // MMA warp, loader warp, kGroups x 4 epilogue warps
+constexpr int kPD = 2;        // cp.async prefetch distance, in the group's own items
+constexpr int kRing = 3;      // x slots per group (> kPD: an item's slot outlives its fix-up)
 
 template <int SUB>
 struct TcShape {
@@ -87,13 +88,14 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 constexpr uint32_t kSuspendNs = 1000000;
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
-    for (uint64_t spin = 0;; ++spin) {
+    const long long t0 = clock64();
+    for (;;) {
         // suspend (woken by the phase flip) instead of busy polling: spinning warps steal
         // issue slots from the epilogue warps that share their SM sub-partition
         asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
                      : "=r"(done) : "r"(smem_u32(bar)), "r"(parity), "r"(kSuspendNs) : "memory");
         if (done) return;
-        if (spin > (1ull << 26)) __trap();  // seconds of waiting: a hang
+        if (clock64() - t0 > 4000000000ll) __trap();  // ~2 s of waiting: a lost arrival
     }
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -162,7 +164,7 @@ __device__ __forceinline__ float exact_score(const float (&x)[SUB], const float 
 struct TcSmemHdr {
     uint64_t b_full[2], b_empty[2];
     uint64_t a_full[kNA];
-    uint64_t t_full[2], t_empty[2];
+    uint64_t t_full[4], t_empty[4];  // by item & 3 (TMEM buffer item & 1): a waiter is never 2 phases off
     uint32_t tmem_base;
 };
 
@@ -197,7 +199,8 @@ struct TcSmem {
     static constexpr size_t oA = oB + 2 * (size_t)S::kBBytes;
     static constexpr size_t oC = oA + kNA * (size_t)S::kABytes;
     static constexpr size_t oX = oC + 2 * (size_t)kCFloats * 4;
-    static constexpr size_t oG = oX + 2 * kRing * (size_t)kXBytes;  // guard constants (2 m floats)
+    static constexpr size_t oS = oX + kGroups * kRing * (size_t)kXBytes;  // block-minima scratch [kGroups][32][kTM]
+    static constexpr size_t oG = oS + (size_t)kGroups * 32 * kTM * 4;        // guard constants (2 m floats)
     static size_t total(int m) { return oG + ((size_t)2 * m * 4 + 15) / 16 * 16 + sizeof(TcSmemHdr) + 16; }
 };
 
@@ -222,6 +225,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
     float *sC = reinterpret_cast<float *>(smem_raw + L::oC);
     unsigned char *sX = smem_raw + L::oX;
     float *sGuard = reinterpret_cast<float *>(smem_raw + L::oG);
+    float *sScr = reinterpret_cast<float *>(smem_raw + L::oS);
     TcSmemHdr *H = reinterpret_cast<TcSmemHdr *>(smem_raw + L::oG + ((size_t)2 * m * 4 + 15) / 16 * 16);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -232,7 +236,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&H->b_full[i], 1);
-            mbar_init(&H->b_empty[i], 1 + 256);  // MMA commit + every epilogue thread (fix-up reads sC)
+            mbar_init(&H->b_empty[i], 1 + 128 * kGroups);  // MMA commit + every epilogue thread (fix-up reads sC)
+        }
+        for (int i = 0; i < 4; ++i) {
             mbar_init(&H->t_full[i], 1);
             mbar_init(&H->t_empty[i], 128);
         }
@@ -261,7 +267,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                         const int as = it % kNA, tb = it & 1;
                         mbar_wait(&H->a_full[as], (it / kNA) & 1);
                         if (stamp && it < kStampItems) stamp[it * 8 + 0] = clock64();
-                        mbar_wait(&H->t_empty[tb], ((it >> 1) & 1) ^ 1);
+                        if (it >= 2) mbar_wait(&H->t_empty[(it - 2) & 3], ((it - 2) >> 2) & 1);  // buffer tb drained
                         if (stamp && it < kStampItems) stamp[it * 8 + 1] = clock64();
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
@@ -271,7 +277,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                             const uint64_t db = make_desc(b0 + 2 * s * 128, 128, S::kRowGroupBytes);
                             if (!(probe & 2)) mma_tf32(tmem + tb * kN, da, db, s > 0);
                         }
-                        mma_commit(&H->t_full[tb]);  // also frees A stage `as` for the group's item it + 4
+                        mma_commit(&H->t_full[it & 3]);  // also frees A stage `as` for item it + kGroups
                         if (stamp && it < kStampItems) stamp[it * 8 + 2] = clock64();
                     }
                     mma_commit(&H->b_empty[jb]);
@@ -295,17 +301,18 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             }
         }
     } else {
-        // ---------------- epilogue + A producer: two groups of 4 warps ----------------
-        // Group e owns the items with (item & 1) == e and TMEM buffer e.  Thread (q, lane)
+        // ---------------- epilogue + A producer: kGroups groups of 4 warps ----------------
+        // Group e owns the items with item % kGroups == e (TMEM buffer item & 1).  Thread (q, lane)
         // owns tile row r = 32 q + lane: it reads that TMEM lane, and it also writes that
-        // row of the A operand of the group's next item (item + 2) and prefetches the
+        // row of the A operand of the group's next item (item + kGroups) and prefetches the
         // row's x kPD owned items ahead into the group's x ring.
-        const int e = (warp - 2) >> 2;
+        const int e = (warp - 2) >> 2;  // group: items it with it % kGroups == e
         const int q = warp & 3;
         const int r = 32 * q + lane;
+        float *scratch = sScr + (size_t)e * 32 * kTM + r;  // this thread's block minima, [32][kTM]
         constexpr float kE = (float)((4.0 / 4194304.0 + S::kSteps / 4194304.0 * (1.0 + 1.0 / 1024.0) + (SUB + 1) / 16777216.0) * 1.01);
         auto ring = [&](uint32_t item) -> unsigned char * {  // x slot of one of the group's items
-            return sX + ((size_t)e * kRing + (item >> 1) % kRing) * L::kXBytes + r * SUB * sizeof(TIn);
+            return sX + ((size_t)e * kRing + (item / kGroups) % kRing) * L::kXBytes + r * SUB * sizeof(TIn);
         };
         auto prefetch = [&](const ItemIter &pi, uint32_t item) {
             const int64_t row = pi.tile() * kTM + r;
@@ -378,32 +385,32 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
         };
 
         ItemIter ii(blockIdx.x, ngroups, ntiles, m);   // current item
-        ItemIter ic = ii, ip = ii;                      // conversion (item + 2) / prefetch (item + 2 kPD)
-        // prologue: stage x for this group's first kPD items, convert the first one
+        ItemIter ic = ii, ip = ii;  // conversion (item + kGroups) / prefetch (item + kGroups kPD)
+        // prologue: stage x for this group's first kPD items, convert its first one
         uint32_t ipi = 0, ici = 0;
-        for (; ipi < (uint32_t)(2 * kPD); ++ipi, ip.next(gridDim.x))
-            if ((int)(ipi & 1) == e) prefetch(ip, ipi);
+        for (; ipi < (uint32_t)(kGroups * kPD); ++ipi, ip.next(gridDim.x))
+            if ((int)(ipi % kGroups) == e) prefetch(ip, ipi);
         float norm_cur = 0.f;
-        if (ic.valid() && e == 0) { cp_async_wait<kPD - 1>(); norm_cur = convert(0); }
-        ic.next(gridDim.x); ++ici;
-        if (ic.valid() && e == 1) { cp_async_wait<kPD - 1>(); norm_cur = convert(1); }
-        ic.next(gridDim.x); ++ici;   // ic now points at item 2
+        for (; ici < (uint32_t)kGroups; ++ici, ic.next(gridDim.x))
+            if ((int)ici == e && ic.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(ici); }
+        // ic now points at item kGroups
 
         for (uint32_t it = 0; ii.valid(); ++it, ii.next(gridDim.x), ic.next(gridDim.x), ip.next(gridDim.x), ++ici, ++ipi) {
             if (ii.t == 0 && it > 0) release_pair(ii.jt - 1);  // done with the previous pair's sC
-            if ((int)(it & 1) != e) continue;
+            if ((int)(it % kGroups) != e) continue;
+            const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
             const int j = ii.j;
-            mbar_wait(&H->t_full[e], (it >> 1) & 1);
+            mbar_wait(&H->t_full[it & 3], (it >> 2) & 1);
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 5] = clock64();
             tc_fence_after();
-            float bm[32], cls[8];
+            float cls[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) cls[c] = pos_inf_f();
 #pragma unroll
             for (int ch = 0; ch < 4 && !(probe & 1); ++ch) {
                 uint32_t v[64];
-                tmem_ld64(tmem + ((uint32_t)(32 * q) << 16) + e * kN + ch * 64, v);
+                tmem_ld64(tmem + ((uint32_t)(32 * q) << 16) + tb * kN + ch * 64, v);
 #define SV(i) __uint_as_float(v[(i)])
                 if (probe & 8) {
                     cls[ch] = __fadd_rn(SV(0), SV(63));
@@ -416,14 +423,14 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         const int o = 16 * bp + 8 * hh;
-                        bm[8 * ch + 2 * bp + hh] = fmin3(fmin3(SV(o), SV(o + 1), SV(o + 2)),
-                                                         fmin3(SV(o + 3), SV(o + 4), SV(o + 5)), fminf(SV(o + 6), SV(o + 7)));
+                        scratch[(8 * ch + 2 * bp + hh) * kTM] = fmin3(fmin3(SV(o), SV(o + 1), SV(o + 2)),
+                                                                     fmin3(SV(o + 3), SV(o + 4), SV(o + 5)), fminf(SV(o + 6), SV(o + 7)));
                     }
                 }
 #undef SV
             }
             tc_fence_before();
-            mbar_arrive(&H->t_empty[e]);
+            mbar_arrive(&H->t_empty[it & 3]);
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 6] = clock64();
             // the group's next item: stage its x prefetch and write its A operand now, so
             // its MMA can start as soon as the other group's item is done
@@ -435,6 +442,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             }
             const float xnorm = norm_cur;
             norm_cur = norm_next;
+            float bm[32];
+#pragma unroll
+            for (int b = 0; b < 32; ++b) bm[b] = (probe & 1) ? pos_inf_f() : scratch[b * kTM];
             // Final selection on the FMA pipe: ind(x) = sat(1 - (x - m1) * 2^151) is exactly 1
             // when x == m1 and exactly 0 otherwise (also for NaN/inf), so the winner's index is
             // sum(ind * i), the number of minima is sum(ind) (a tie -> flag), and the runner-up
@@ -481,7 +491,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                 while (mask) {
                     const int src = __ffs(mask) - 1;
                     mask &= mask - 1;
-                    const TIn *xr = reinterpret_cast<const TIn *>(sX + ((size_t)e * kRing + (it >> 1) % kRing) * L::kXBytes) +
+                    const TIn *xr = reinterpret_cast<const TIn *>(sX + ((size_t)e * kRing + (it / kGroups) % kRing) * L::kXBytes) +
                                     (32 * q + src) * SUB;
                     float xv[SUB];
 #pragma unroll
