@@ -286,6 +286,35 @@ int cspq_encode_vecs_file(const char *in_path, int32_t in_format, const char *ou
                           int64_t batch_rows, int32_t n_streams, int32_t device, int64_t *n_rows,
                           int64_t *err);
 
+/* ---------------------------------------------------------------------------
+ * Flat ADC search and its exact ground truth (evaluation.py), query time.
+ * ------------------------------------------------------------------------- */
+
+/* tables (nq, m, k) float32: tables[q, j, l] = ||c_jl - q_j||^2 summed like
+ * numpy's einsum("kt,kt->k") (evaluation.py:66-88; bit-identical for
+ * sub <= 12).  Q (nq, d) row-major float32. */
+int cspq_adc_tables(const float *Q, int64_t nq, int32_t d, const float *CB, int32_t m, int32_t k,
+                    int32_t sub, float *tables, void *stream);
+
+/* scores (nq, n) float32: table sums over the m chunks in chunk order from
+ * 0.0 (adc_scores, evaluation.py:91-96); codes (n, m) uint8 (k <= 256) or
+ * uint16. */
+int cspq_adc_scores(const float *tables, int64_t nq, const void *codes, int64_t n, int32_t m,
+                    int32_t k, float *scores, void *stream);
+
+/* Per row q of values (nq, n) (float32: value_bytes 4, float64: 8): the
+ * topn smallest (value, index) pairs in lexsort order -- ties toward the
+ * smaller index, NaN last (evaluation.py:99-103, 124-128).  indices (nq,
+ * topn) int64, top_values (nq, topn).  1 <= topn <= min(n, 1024). */
+int cspq_topn(const void *values, int32_t value_bytes, int64_t nq, int64_t n, int32_t topn,
+              int64_t *indices, void *top_values, void *stream);
+
+/* Ground-truth distances (exact_topn, evaluation.py:114-129): norms (n)
+ * float64 = ||x||^2, dist (nq, n) float64 = norms - 2 q.x, float32 inputs
+ * widened, float64 fused products in ascending t. */
+int cspq_exact_distances(const float *queries, int64_t nq, const float *db, int64_t n, int32_t d,
+                         double *norms, double *dist, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,12 +71,14 @@ from .io import (
     write_fvecs,
     write_ivecs,
 )
+from .evaluation import EvalReport, adc_search, adc_search_batched, evaluate, exact_topn, mse_of, reconstruct
 from ._device import pinned_empty
 from ._native import NativeUnavailable
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "EvalReport", "adc_search", "adc_search_batched", "evaluate", "exact_topn", "mse_of", "reconstruct",
     "crc32_device", "encode_file", "read_bvecs", "read_codebooks", "read_codes", "read_fvecs", "read_ivecs",
     "synth_dataset", "write_bvecs", "write_codebooks", "write_codes", "write_fvecs", "write_ivecs",
     "CHUNK_MAJOR", "VECTOR_MAJOR", "Codebook", "CodebookSet", "ConfigError", "CorruptionError",

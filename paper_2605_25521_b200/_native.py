@@ -58,6 +58,10 @@ _SIGS = {
     "cspq_crc32_device": ([_vp, _i64, ctypes.c_uint32, _vp, _vp, _vp], _i32),
     "cspq_crc32_combine": ([ctypes.c_uint32, ctypes.c_uint32, _i64], ctypes.c_uint32),
     "cspq_unpack_vecs": ([_vp, _i64, _i32, _i32, _i32, _i64, _vp, _vp, _vp], _i32),
+    "cspq_adc_tables": ([_vp, _i64, _i32, _vp, _i32, _i32, _i32, _vp, _vp], _i32),
+    "cspq_adc_scores": ([_vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp], _i32),
+    "cspq_topn": ([_vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp], _i32),
+    "cspq_exact_distances": ([_vp, _i64, _vp, _i64, _i32, _vp, _vp, _vp], _i32),
     "cspq_encode_vecs_file": ([ctypes.c_char_p, _i32, ctypes.c_char_p, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
                                _i32, _i64, _i32, _i32, _vp, _vp], _i32),
 }

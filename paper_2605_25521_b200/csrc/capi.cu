@@ -33,6 +33,13 @@ int encode_with_scores(const void *X, int in_dtype, int64_t n, int64_t xrs, cons
                        int m, int k, int sub, int32_t *codes, float *best, int variant, cudaStream_t st);
 size_t lloyd_workspace_bytes(int64_t n, int m, int sub, int k);
 size_t crc32_workspace_bytes(int64_t n);
+int adc_tables(const float *Q, int64_t nq, int d, const float *CB, int m, int k, int sub, float *T, cudaStream_t st);
+int adc_scores(const float *T, int64_t nq, const void *codes, int code_bytes, int64_t n, int m, int k, float *S,
+               cudaStream_t st);
+int topn_select(const void *vals, int val_bytes, int64_t nq, int64_t n, int topn, int64_t *idx, void *out_vals,
+                cudaStream_t st);
+int gt_distances(const float *Qm, int64_t nq, const float *X, int64_t n, int d, double *nrm, double *D,
+                 cudaStream_t st);
 int crc32_device_api(const void *data, int64_t n, uint32_t crc_in, uint32_t *crc_out, void *ws, cudaStream_t st);
 uint32_t crc32_combine_host(uint32_t crc1, uint32_t crc2, int64_t len2);
 int unpack_vecs(const void *records, int64_t n, int d, int value_bytes, int check_finite, int64_t off0, void *rows,
@@ -333,6 +340,43 @@ int cspq_encode_host(const void *X_host, int32_t in_dtype, int64_t n, int32_t d,
 }
 
 size_t cspq_crc32_workspace_bytes(int64_t n) { return crc32_workspace_bytes(n); }
+
+int cspq_adc_tables(const float *Q, int64_t nq, int32_t d, const float *CB, int32_t m, int32_t k, int32_t sub,
+                    float *tables, void *stream) {
+    int rc = check_shape(nq, m, k, sub);
+    if (rc) return rc;
+    CSPQ_REQUIRE(d == m * sub, CSPQ_E_CONFIG, "query length %d does not match d=%d", d, m * sub);
+    if (nq == 0) return CSPQ_OK;
+    CSPQ_REQUIRE(Q && CB && tables, CSPQ_E_CONFIG, "null pointer");
+    return adc_tables(Q, nq, d, CB, m, k, sub, tables, as_stream(stream));
+}
+
+int cspq_adc_scores(const float *tables, int64_t nq, const void *codes, int64_t n, int32_t m, int32_t k, float *scores,
+                    void *stream) {
+    int rc = check_shape(n, m, k, 1);
+    if (rc) return rc;
+    CSPQ_REQUIRE(nq >= 0, CSPQ_E_CONFIG, "nq must be >= 0");
+    if (nq == 0 || n == 0) return CSPQ_OK;
+    CSPQ_REQUIRE(tables && codes && scores, CSPQ_E_CONFIG, "null pointer");
+    return adc_scores(tables, nq, codes, k <= 256 ? 1 : 2, n, m, k, scores, as_stream(stream));
+}
+
+int cspq_topn(const void *values, int32_t value_bytes, int64_t nq, int64_t n, int32_t topn, int64_t *indices,
+              void *top_values, void *stream) {
+    CSPQ_REQUIRE(value_bytes == 4 || value_bytes == 8, CSPQ_E_CONFIG, "value_bytes must be 4 (f32) or 8 (f64)");
+    CSPQ_REQUIRE(nq >= 0 && n >= 0, CSPQ_E_CONFIG, "bad shape");
+    if (nq == 0) return CSPQ_OK;
+    CSPQ_REQUIRE(values && indices && top_values, CSPQ_E_CONFIG, "null pointer");
+    return topn_select(values, value_bytes, nq, n, topn, indices, top_values, as_stream(stream));
+}
+
+int cspq_exact_distances(const float *queries, int64_t nq, const float *db, int64_t n, int32_t d, double *norms,
+                         double *dist, void *stream) {
+    CSPQ_REQUIRE(nq >= 0 && n >= 0 && d >= 1, CSPQ_E_CONFIG, "bad shape");
+    if (nq == 0 || n == 0) return CSPQ_OK;
+    CSPQ_REQUIRE(queries && db && norms && dist, CSPQ_E_CONFIG, "null pointer");
+    return gt_distances(queries, nq, db, n, d, norms, dist, as_stream(stream));
+}
 
 int cspq_crc32_device(const void *data, int64_t n, uint32_t crc_in, uint32_t *crc_out, void *workspace,
                       void *stream) {

@@ -288,6 +288,38 @@ def io_cases():
     return out
 
 
+def eval_cases():
+    """Reference evaluation.py outputs: tables / scores bits, ADC top-N, exact
+    ground truth, mse_of and evaluate() reports."""
+    from cspq import bulk, core, evaluation as ev
+    out = {}
+    rng = np.random.default_rng(20260303)
+    cases = []
+    # (name, n, d, m, k, dup): dup > 0 duplicates rows to force exact score / distance ties
+    for name, n, m, sub, k, dup in (("e_s8", 3000, 8, 8, 256, 0), ("e_s4_ties", 2000, 8, 4, 64, 400),
+                                    ("e_k1000", 1500, 4, 8, 1000, 0), ("e_s16", 1200, 2, 16, 256, 0)):
+        d = m * sub
+        X = rng.standard_normal((n, d)).astype(np.float32)
+        if dup:
+            X[-dup:] = X[:dup]
+        Q = np.concatenate([rng.standard_normal((14, d)).astype(np.float32), X[:6] + 0.0]).astype(np.float32)
+        rm = np.stack([X[rng.choice(n, k, replace=k > n), j * sub:(j + 1) * sub] for j in range(m)])
+        rm = (rm + rng.normal(0, 0.05, rm.shape)).astype(np.float32)
+        cbs = [core.Codebook.from_rowmajor(j, rm[j]) for j in range(m)]
+        codes = bulk.encode_dataset(X, bulk.CodebookSet.from_codebooks(cbs))
+        out[f"{name}/X"], out[f"{name}/Q"], out[f"{name}/rowmajor"], out[f"{name}/codes"] = X, Q, rm, codes.codes
+        out[f"{name}/tables0"] = ev.adc_tables(Q[0], cbs)
+        out[f"{name}/scores0"] = ev.adc_scores(out[f"{name}/tables0"], codes)
+        idx, dist = zip(*[ev.adc_search(q, codes, cbs, 10) for q in Q])
+        out[f"{name}/adc_idx"], out[f"{name}/adc_dist"] = np.stack(idx), np.stack(dist)
+        out[f"{name}/gt"] = ev.exact_topn(Q, X, 10)
+        out[f"{name}/mse"] = np.float64(ev.mse_of(X, codes, cbs))
+        rep = ev.evaluate(core.VectorDataset(data=X), core.VectorDataset(data=Q), cbs, topn=10, codes=codes)
+        out[f"{name}/recall"] = np.float64(rep.recall_at_n)
+        out[f"{name}/recon7"] = ev.reconstruct(codes.codes[7], cbs)
+    return out
+
+
 def main():
     bulk, core, kernels, training = _ref()
     np.savez_compressed(os.path.join(HERE, "encode_golden.npz"), **encode_cases(bulk, core, kernels))
@@ -295,6 +327,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "train_golden.npz"), **train_cases(core, training))
     np.savez_compressed(os.path.join(HERE, "pairwise_golden.npz"), **pairwise_cases())
     np.savez_compressed(os.path.join(HERE, "io_golden.npz"), **io_cases())
+    np.savez_compressed(os.path.join(HERE, "eval_golden.npz"), **eval_cases())
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
