@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--mode", default="auto", choices=["auto", "exact", "guarded"])
     p.add_argument("--e2e-rows", type=int, default=0,
                    help="rows per rank through the host API (0 = 2M, or the whole config for c5)")
+    p.add_argument("--streams", type=int, default=0, help="host pipeline streams (0 = 3, or 6 for c5)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -243,7 +244,7 @@ def main():
         Xh = P.pinned_empty((ne, cfg.d), np.uint8 if cfg.dtype == "u8" else np.float32)
         Xh[:] = X[:ne].cpu().numpy()
         codes_h = P.pinned_empty((ne, cfg.m), np.uint8)
-        eplan = P.ExecutionPlan(mode=args.mode, batch_rows=batch_rows, streams=3)
+        eplan = P.ExecutionPlan(mode=args.mode, batch_rows=batch_rows, streams=args.streams or (6 if cfg.batch else 3))
         nb = (ne + batch_rows - 1) // batch_rows
         bms = np.zeros(nb, np.float64)
         P.encode_dataset_host(Xh, cs, eplan, out=codes_h)  # warm the pipeline
@@ -263,11 +264,12 @@ def main():
         lat = np.concatenate(lat)
         e2e = {"value": e2e_val, "unit": "vectors/s", "h2d_bytes_per_step": int(ne * cfg.d * cfg.elem_bytes) * ws,
                "d2h_bytes_per_step": int(ne * cfg.m) * ws, "rows_per_gpu": ne, "batch_rows": batch_rows,
+               "streams": eplan.streams,
                "batch_latency_ms": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
                                     "batches": int(lat.shape[0]),
                                     "def": "device events: H2D start -> D2H end of one batch (3 batches in flight)"},
                "h2d_GBps": ne * cfg.d * cfg.elem_bytes * args.steps / float(el.item()) / 1e9,
-               "path": "encode_dataset_host (pinned numpy -> cspq_encode_host: 3-stream H2D/encode/D2H pipeline)"}
+               "path": "encode_dataset_host (pinned numpy -> cspq_encode_host: multi-stream H2D/encode/D2H pipeline)"}
 
     # ---- roofline of the encode kernel ----
     flops_launch = rows * cfg.flops_per_vec()
