@@ -58,6 +58,10 @@ constexpr int kG = 8;        // tiles per row group (codebook image reuse)
 constexpr int kGroups = 3;   // epilogue groups: item it belongs to group it % kGroups
 constexpr int kNA = kGroups; // A-operand stages (a group writes item it + kGroups into item it's stage)
 constexpr int kThreads = 64 + 128 * kGroups;  // MMA warp, loader warp, kGroups x 4 epilogue warps
+constexpr int kNC = 1;        // accumulator chunks per item (N = 256 / kNC per MMA, own commit + barriers):
+                              // MMA and scan overlap chunk by chunk; measured on c3: 1 = 2.16e8 vec/s,
+                              // 2 = 2.04e8, 4 = 1.44e8 (an N=64 MMA costs almost what an N=256 one does)
+constexpr int kCW = 256 / kNC;  // chunk width in TMEM columns (a multiple of 64: one tcgen05.ld x64)
 constexpr int kPD = 2;        // cp.async prefetch distance, in the group's own items
 constexpr int kRing = 3;      // x slots per group (> kPD: an item's slot outlives its fix-up)
 
@@ -119,16 +123,16 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 
-__host__ __device__ constexpr uint32_t make_idesc() {
+__host__ __device__ constexpr uint32_t make_idesc(int n = kN) {
     // kind::tf32: D f32 (bit 4), A tf32 (2 << 7), B tf32 (2 << 10), K-major A/B,
     // N >> 3 at [17, 23), M >> 4 at [24, 29)
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-                 "l"(da), "l"(db), "r"(make_idesc()), "r"(accumulate) : "memory");
+                 "l"(da), "l"(db), "r"(make_idesc(kCW)), "r"(accumulate) : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -164,7 +168,7 @@ __device__ __forceinline__ float exact_score(const float (&x)[SUB], const float 
 struct TcSmemHdr {
     uint64_t b_full[2], b_empty[2];
     uint64_t a_full[kNA];
-    uint64_t t_full[4], t_empty[4];  // by item & 3 (TMEM buffer item & 1): a waiter is never 2 phases off
+    uint64_t t_full[4][kNC], t_empty[4][kNC];  // [item & 3][chunk] (TMEM buffer item & 1): never 2 phases off
     uint32_t tmem_base;
 };
 
@@ -239,8 +243,10 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             mbar_init(&H->b_empty[i], 1 + 128 * kGroups);  // MMA commit + every epilogue thread (fix-up reads sC)
         }
         for (int i = 0; i < 4; ++i) {
-            mbar_init(&H->t_full[i], 1);
-            mbar_init(&H->t_empty[i], 128);
+            for (int c = 0; c < kNC; ++c) {
+                mbar_init(&H->t_full[i][c], 1);
+                mbar_init(&H->t_empty[i][c], 128);
+            }
         }
         for (int i = 0; i < kNA; ++i) mbar_init(&H->a_full[i], 128);
         fence_mbar_init();
@@ -267,17 +273,21 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                         const int as = it % kNA, tb = it & 1;
                         mbar_wait(&H->a_full[as], (it / kNA) & 1);
                         if (stamp && it < kStampItems) stamp[it * 8 + 0] = clock64();
-                        if (it >= 2) mbar_wait(&H->t_empty[(it - 2) & 3], ((it - 2) >> 2) & 1);  // buffer tb drained
-                        if (stamp && it < kStampItems) stamp[it * 8 + 1] = clock64();
-                        tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
+                        for (int c = 0; c < kNC; ++c) {
+                            // chunk c of buffer tb drained by the scan of item it - 2
+                            if (it >= 2) mbar_wait(&H->t_empty[(it - 2) & 3][c], ((it - 2) >> 2) & 1);
+                            if (stamp && c == 0 && it < kStampItems) stamp[it * 8 + 1] = clock64();
+                            tc_fence_after();
+                            const uint32_t bc = b0 + (uint32_t)(c * (kCW / 8) * S::kRowGroupBytes);  // centroids c kCW ..
 #pragma unroll
-                        for (int s = 0; s < S::kSteps; ++s) {
-                            const uint64_t da = make_desc(a0 + 2 * s * 128, 128, S::kRowGroupBytes);
-                            const uint64_t db = make_desc(b0 + 2 * s * 128, 128, S::kRowGroupBytes);
-                            if (!(probe & 2)) mma_tf32(tmem + tb * kN, da, db, s > 0);
+                            for (int s = 0; s < S::kSteps; ++s) {
+                                const uint64_t da = make_desc(a0 + 2 * s * 128, 128, S::kRowGroupBytes);
+                                const uint64_t db = make_desc(bc + 2 * s * 128, 128, S::kRowGroupBytes);
+                                if (!(probe & 2)) mma_tf32(tmem + tb * kN + c * kCW, da, db, s > 0);
+                            }
+                            mma_commit(&H->t_full[it & 3][c]);  // the last one also frees A stage `as`
                         }
-                        mma_commit(&H->t_full[it & 3]);  // also frees A stage `as` for item it + kGroups
                         if (stamp && it < kStampItems) stamp[it * 8 + 2] = clock64();
                     }
                     mma_commit(&H->b_empty[jb]);
@@ -401,16 +411,24 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
             const int j = ii.j;
-            mbar_wait(&H->t_full[it & 3], (it >> 2) & 1);
-            if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 5] = clock64();
-            tc_fence_after();
             float cls[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) cls[c] = pos_inf_f();
 #pragma unroll
             for (int ch = 0; ch < 4 && !(probe & 1); ++ch) {
+                constexpr int kLdPerChunk = kCW / 64;
+                const int c = ch / kLdPerChunk;
+                if (ch % kLdPerChunk == 0) {
+                    mbar_wait(&H->t_full[it & 3][c], (it >> 2) & 1);
+                    if (stamp && r == 0 && ch == 0 && it < kStampItems) stamp[it * 8 + 5] = clock64();
+                    tc_fence_after();
+                }
                 uint32_t v[64];
                 tmem_ld64(tmem + ((uint32_t)(32 * q) << 16) + tb * kN + ch * 64, v);
+                if (ch % kLdPerChunk == kLdPerChunk - 1) {  // chunk c is in registers: hand it back
+                    tc_fence_before();
+                    mbar_arrive(&H->t_empty[it & 3][c]);
+                }
 #define SV(i) __uint_as_float(v[(i)])
                 if (probe & 8) {
                     cls[ch] = __fadd_rn(SV(0), SV(63));
@@ -429,8 +447,12 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                 }
 #undef SV
             }
-            tc_fence_before();
-            mbar_arrive(&H->t_empty[it & 3]);
+            if (probe & 1) {  // (timing probe: no TMEM reads; still walk the barriers)
+                for (int c = 0; c < kNC; ++c) {
+                    mbar_wait(&H->t_full[it & 3][c], (it >> 2) & 1);
+                    mbar_arrive(&H->t_empty[it & 3][c]);
+                }
+            }
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 6] = clock64();
             // the group's next item: stage its x prefetch and write its A operand now, so
             // its MMA can start as soon as the other group's item is done
