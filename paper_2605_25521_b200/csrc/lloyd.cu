@@ -36,7 +36,7 @@ constexpr uint64_t kMagic = 0x43535051424C4C59ull;
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
-    int64_t header, leaves, hist, cnt, start, perm, sq, resid, leafsum, cn;
+    int64_t header, leaves, nodes, ntmp, nodeval, hist, cnt, start, perm, sq, resid, leafsum, cn;
     // train-loop state
     int64_t counts, sums, obj, prev, state, empties, nempty, assign_it;
     // float32 copy of float64 points (final pass), k-means++ scratch
@@ -50,6 +50,9 @@ struct WsLayout {
         auto take = [&](int64_t bytes) { int64_t r = o; o = align_up(o + bytes, 256); return r; };
         header = take(256);
         leaves = take(16 * maxleaves);
+        nodes = take(8 * maxleaves + 4 * 80);   // internal nodes (left, right) by height + level offsets
+        ntmp = take(12 * maxleaves);            // construction scratch (left, right, height)
+        nodeval = take(8 * (int64_t)m * maxleaves);
         hist = take(4 * (int64_t)m * nch * k);
         cnt = take(4 * (int64_t)m * k);
         start = take(4 * (int64_t)m * k);
@@ -79,14 +82,20 @@ struct WsHeader {
     uint64_t magic;
     int64_t leaves_for;  // range length the leaf table describes
     int64_t nleaves;
+    int64_t nlevels;     // heights 1 .. nlevels of the internal nodes
 };
 
 // ---------------------------------------------------------------- pairwise tree
 // Leaves of numpy's pairwise summation of a length-n range, in order
 // (pairwise_sum: n <= 128 is a leaf; otherwise split at n2 = n/2 - (n/2)%8).
-__global__ void leaves_kernel(int64_t n, int64_t *leaves, WsHeader *hdr) {
+// Also the internal nodes of that recursion (node = left + right, exactly numpy's order),
+// grouped by height so that a CTA can evaluate them level by level.  Node ids: leaves are
+// 0 .. nl-1 (in order), internal nodes nl .. in construction order.  Built once per n.
+__global__ void leaves_kernel(int64_t n, int64_t *leaves, int32_t *nodes, int32_t *ntmp, int64_t maxleaves,
+                              WsHeader *hdr) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (hdr->magic == kMagic && hdr->leaves_for == n) return;
+    // pass 1: leaves in order
     struct F { int64_t lo, len; };
     F st[96];
     int sp = 0;
@@ -100,9 +109,70 @@ __global__ void leaves_kernel(int64_t n, int64_t *leaves, WsHeader *hdr) {
         st[sp++] = {f.lo + n2, f.len - n2};  // right pushed first: left is visited first
         st[sp++] = {f.lo, n2};
     }
+    // pass 2: post-order walk giving every internal node (left id, right id, height)
+    struct G { int64_t len; int stage; int32_t left, lh; };
+    G gs[96];
+    int gp = 0;
+    int32_t next_leaf = 0, next_node = (int32_t)nl, ret = 0, rh = 0, maxh = 0;
+    gs[0] = {n, 0, 0, 0};
+    for (;;) {
+        G &g = gs[gp];
+        if (g.stage == 0) {
+            if (g.len <= 128) {
+                ret = next_leaf++;
+                rh = 0;
+                if (gp == 0) break;
+                --gp;
+                continue;
+            }
+            int64_t n2 = g.len / 2;
+            n2 -= n2 % 8;
+            g.stage = 1;
+            gs[++gp] = {n2, 0, 0, 0};
+        } else if (g.stage == 1) {
+            g.left = ret;
+            g.lh = rh;
+            g.stage = 2;
+            int64_t n2 = g.len / 2;
+            n2 -= n2 % 8;
+            gs[++gp] = {g.len - n2, 0, 0, 0};
+        } else {
+            const int32_t id = next_node++, h = 1 + (g.lh > rh ? g.lh : rh);
+            int32_t *t = ntmp + 3 * (int64_t)(id - nl);
+            t[0] = g.left; t[1] = ret; t[2] = h;
+            maxh = h > maxh ? h : maxh;
+            ret = id;
+            rh = h;
+            if (gp == 0) break;
+            --gp;
+        }
+    }
+    // counting sort of the internal nodes by height: nodes = [(left, right)...], level
+    // offsets after them (level h occupies [off[h-1], off[h]))
+    const int64_t ni = next_node - nl;
+    int32_t *off = nodes + 2 * maxleaves;
+    for (int h = 0; h <= maxh; ++h) off[h] = 0;
+    for (int64_t i = 0; i < ni; ++i) ++off[ntmp[3 * i + 2]];
+    int32_t run = 0;
+    for (int h = 1; h <= maxh; ++h) { const int32_t c = off[h]; off[h] = run; run += c; }
+    off[0] = 0;
+    // off[h] is now the start of level h; place, then turn starts into ends
+    for (int64_t i = 0; i < ni; ++i) {
+        const int32_t h = ntmp[3 * i + 2];
+        const int32_t pos = off[h]++;
+        nodes[2 * (int64_t)pos] = ntmp[3 * i];
+        nodes[2 * (int64_t)pos + 1] = ntmp[3 * i + 1];
+        ntmp[3 * i + 2] = pos;  // construction index -> sorted slot
+    }
+    // children that are internal nodes: construction id -> nl + sorted slot
+    for (int64_t p = 0; p < 2 * ni; ++p) {
+        const int32_t c = nodes[p];
+        if (c >= nl) nodes[p] = (int32_t)nl + ntmp[3 * (int64_t)(c - nl) + 2];
+    }
     hdr->magic = kMagic;
     hdr->leaves_for = n;
     hdr->nleaves = nl;
+    hdr->nlevels = maxh;  // off[h] = end of level h; level 1 starts at 0
 }
 
 // numpy leaf sum: <8 sequential from 0.0; else 8 accumulators, fixed combine, tail
@@ -137,45 +207,34 @@ __global__ void leafsum_kernel(const double *vals, int64_t vstride, int64_t begi
         leafsum[(int64_t)j * maxleaves + l] = leaf_sum(vals + (int64_t)j * vstride + begin + leaves[2 * l], leaves[2 * l + 1]);
 }
 
-// recombine leaves along the same recursion (one thread per subspace)
-__global__ void combine_kernel(int64_t n, int m, const int32_t *state, const double *leafsum,
-                               int64_t maxleaves, double *out) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= m) return;
+// evaluate the internal nodes level by level (one CTA per subspace); node ids are
+// translated to storage: id < nl -> leafsum, else nodeval[id - nl] at its sorted slot
+__global__ void combine_levels_kernel(int m, const int32_t *state, const double *leafsum, int64_t maxleaves,
+                                      const int32_t *nodes, const WsHeader *hdr, double *nodeval, double *out) {
+    const int j = blockIdx.x;
     if (state && !state[j]) return;
+    const int64_t nl = hdr->nleaves;
+    const int H = (int)hdr->nlevels;
     const double *ls = leafsum + (int64_t)j * maxleaves;
-    struct F { int64_t len, n2; int stage; double left; };
-    F st[96];
-    int sp = 0;
-    int64_t leaf = 0;
-    double ret = 0.0;
-    st[0] = {n, 0, 0, 0.0};
-    for (;;) {
-        F &f = st[sp];
-        if (f.stage == 0) {
-            if (f.len <= 128) {
-                ret = ls[leaf++];
-                if (sp == 0) break;
-                --sp;
-                continue;
-            }
-            int64_t n2 = f.len / 2;
-            n2 -= n2 % 8;
-            f.n2 = n2;
-            f.stage = 1;
-            st[++sp] = {n2, 0, 0, 0.0};
-        } else if (f.stage == 1) {
-            f.left = ret;
-            f.stage = 2;
-            const int64_t rl = f.len - f.n2;
-            st[++sp] = {rl, 0, 0, 0.0};
-        } else {
-            ret = __dadd_rn(f.left, ret);
-            if (sp == 0) break;
-            --sp;
-        }
+    double *nv = nodeval + (int64_t)j * maxleaves;
+    if (H == 0) {
+        if (threadIdx.x == 0) out[j] = ls[0];
+        return;
     }
-    out[j] = ret;
+    const int32_t *off = nodes + 2 * maxleaves;  // level ends
+    int32_t lo = 0;
+    for (int h = 1; h <= H; ++h) {
+        const int32_t hi = off[h];
+        for (int32_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+            const int32_t a = nodes[2 * (int64_t)p], b = nodes[2 * (int64_t)p + 1];
+            const double va = a < nl ? ls[a] : nv[a - nl];
+            const double vb = b < nl ? ls[b] : nv[b - nl];
+            nv[p] = __dadd_rn(va, vb);
+        }
+        lo = hi;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[j] = nv[off[H] - 1];  // the root is alone on the top level
 }
 
 // ---------------------------------------------------------------- assignment
@@ -211,25 +270,78 @@ assign_kernel(const TP *__restrict__ P, int64_t n, int k, int sub_rt, const doub
         cnj = scn;
     }
     const TP *Pj = P + (int64_t)j * n * sub;
+    if constexpr (SUBC > 0) {
+        // Two points per thread (each broadcast centroid load feeds both) and four centroids
+        // per step (independent fma chains); every (point, centroid) value is the same
+        // ascending chain as before, d = cn - 2 dot is one rounding either way (2 dot is
+        // exact), and the argmin still compares centroids in index order.
+        constexpr int kPPT = 2;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x * kPPT;
+        for (int64_t i0 = b + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kPPT; i0 < e; i0 += stride) {
+            double x[kPPT][SUBC], best[kPPT];
+            int bi[kPPT];
+#pragma unroll
+            for (int p = 0; p < kPPT; ++p) {
+                const int64_t i = i0 + p < e ? i0 + p : i0;  // a missing second point repeats the first
+#pragma unroll
+                for (int t = 0; t < SUBC; ++t) x[p][t] = (double)Pj[i * SUBC + t];
+                best[p] = 0.0;
+                bi[p] = 0;
+            }
+            int l = 0;
+            for (; l + 4 <= k; l += 4) {
+                double dl[kPPT][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double *c = Cj + (int64_t)(l + u) * SUBC;
+                    double cv[SUBC];
+#pragma unroll
+                    for (int t = 0; t < SUBC; ++t) cv[t] = c[t];
+                    const double cn = cnj[l + u];
+#pragma unroll
+                    for (int p = 0; p < kPPT; ++p) {
+                        double dot = 0.0;
+#pragma unroll
+                        for (int t = 0; t < SUBC; ++t) dot = __fma_rn(x[p][t], cv[t], dot);
+                        dl[p][u] = __fma_rn(-2.0, dot, cn);
+                    }
+                }
+#pragma unroll
+                for (int p = 0; p < kPPT; ++p)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if ((l + u) == 0 || dl[p][u] < best[p]) { best[p] = dl[p][u]; bi[p] = l + u; }
+            }
+            for (; l < k; ++l) {
+                const double *c = Cj + (int64_t)l * SUBC;
+#pragma unroll
+                for (int p = 0; p < kPPT; ++p) {
+                    double dot = 0.0;
+#pragma unroll
+                    for (int t = 0; t < SUBC; ++t) dot = __fma_rn(x[p][t], c[t], dot);
+                    const double d1 = __fma_rn(-2.0, dot, cnj[l]);
+                    if (l == 0 || d1 < best[p]) { best[p] = d1; bi[p] = l; }
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < kPPT; ++p) {
+                const int64_t i = i0 + p;
+                if (i >= e) break;
+                double xx = 0.0;
+#pragma unroll
+                for (int t = 0; t < SUBC; ++t) xx = __dadd_rn(xx, __dmul_rn(x[p][t], x[p][t]));
+                const double v = __dadd_rn(best[p], xx);
+                assign[(int64_t)j * n + i] = bi[p];
+                sq[(int64_t)j * n + i] = (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(v, 0.0)
+            }
+        }
+        return;
+    }
     for (int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
         double best = 0.0;
         int bi = 0;
         double xx = 0.0;
-        if constexpr (SUBC > 0) {
-            double x[SUBC];
-#pragma unroll
-            for (int t = 0; t < SUBC; ++t) x[t] = (double)Pj[i * SUBC + t];
-            for (int l = 0; l < k; ++l) {
-                const double *c = Cj + (int64_t)l * SUBC;
-                double dot = 0.0;
-#pragma unroll
-                for (int t = 0; t < SUBC; ++t) dot = __fma_rn(x[t], c[t], dot);
-                const double dl = __dsub_rn(cnj[l], __dmul_rn(2.0, dot));
-                if (l == 0 || dl < best) { best = dl; bi = l; }
-            }
-#pragma unroll
-            for (int t = 0; t < SUBC; ++t) xx = __dadd_rn(xx, __dmul_rn(x[t], x[t]));
-        } else {
+        {
             const TP *x = Pj + i * sub;
             for (int l = 0; l < k; ++l) {
                 const double *c = Cj + (int64_t)l * sub;
@@ -600,13 +712,15 @@ int pairwise_obj(const double *vals, int64_t vstride, int64_t begin, int64_t len
     WsHeader *hdr = L.at<WsHeader>(ws, L.header);
     int64_t *leaves = L.at<int64_t>(ws, L.leaves);
     double *leafsum = L.at<double>(ws, L.leafsum);
-    leaves_kernel<<<1, 1, 0, st>>>(len, leaves, hdr);
+    int32_t *nodes = L.at<int32_t>(ws, L.nodes);
+    leaves_kernel<<<1, 1, 0, st>>>(len, leaves, nodes, L.at<int32_t>(ws, L.ntmp), L.maxleaves, hdr);
     CSPQ_LAUNCH_CHECK();
     const int64_t maxl = len / 32 + 8;
     dim3 g((unsigned)grid_for(maxl, 128, 64), (unsigned)m);
     leafsum_kernel<<<g, 128, 0, st>>>(vals, vstride, begin, m, state, leaves, hdr, L.maxleaves, leafsum);
     CSPQ_LAUNCH_CHECK();
-    combine_kernel<<<(m + 63) / 64, 64, 0, st>>>(len, m, state, leafsum, L.maxleaves, out);
+    combine_levels_kernel<<<m, 256, 0, st>>>(m, state, leafsum, L.maxleaves, nodes, hdr,
+                                             L.at<double>(ws, L.nodeval), out);
     CSPQ_LAUNCH_CHECK();
     return CSPQ_OK;
 }

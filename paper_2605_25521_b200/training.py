@@ -111,13 +111,18 @@ def lloyd_iterate_batched(points, init, cfg: TrainConfig, dev=None) -> list[KMea
         iters = t.zeros((m,), dtype=t.int32, device=dev)
         N.call("cspq_lloyd_train", ptr(Pd), pf64, n, m, sub, k, ptr(Cd), cfg.max_iters, float(cfg.tol),
                ptr(C32), ptr(asg), ptr(objs), ptr(iters), ptr(ws), stream_ptr(dev))
-        C32h, asgh, objh, ith = (x.cpu().numpy() for x in (C32, asg, objs, iters))
+        # assignments leave as one pinned int64 block (widened on the device); results slice it
+        asg64 = t.empty((m, n), dtype=t.int64, pin_memory=True)
+        asg64.copy_(asg.long(), non_blocking=True)
+        C32h, objh, ith = (x.cpu().numpy() for x in (C32, objs, iters))
+        t.cuda.current_stream(dev).synchronize()
+        asgh = asg64.numpy()
     out = []
     for j in range(m):
         it = int(ith[j])
         out.append(KMeansResult(centroids=np.ascontiguousarray(C32h[j]),
                                 objectives=[float(v) for v in objh[j, :it + 1]],
-                                assignments=asgh[j].astype(np.int64), n_train=n, iterations=it))
+                                assignments=asgh[j], n_train=n, iterations=it))
     return out
 
 
