@@ -238,6 +238,12 @@ __global__ void combine_levels_kernel(int m, const int32_t *state, const double 
 }
 
 // ---------------------------------------------------------------- assignment
+#ifndef CSPQ_LLOYD_PPT
+#define CSPQ_LLOYD_PPT 4  // points per thread in assign_kernel (2x4, 4x2, 4x4, 2x8, 1x8 measured: 4x2 best)
+#endif
+#ifndef CSPQ_LLOYD_U
+#define CSPQ_LLOYD_U 2    // centroids per step in assign_kernel
+#endif
 __global__ void cnorm_kernel(const double *C64, int m, int k, int sub, const int32_t *state, double *cn) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (int64_t)m * k) return;
@@ -275,7 +281,8 @@ assign_kernel(const TP *__restrict__ P, int64_t n, int k, int sub_rt, const doub
         // per step (independent fma chains); every (point, centroid) value is the same
         // ascending chain as before, d = cn - 2 dot is one rounding either way (2 dot is
         // exact), and the argmin still compares centroids in index order.
-        constexpr int kPPT = 2;
+        constexpr int kPPT = CSPQ_LLOYD_PPT;
+        constexpr int kU = CSPQ_LLOYD_U;
         const int64_t stride = (int64_t)gridDim.x * blockDim.x * kPPT;
         for (int64_t i0 = b + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kPPT; i0 < e; i0 += stride) {
             double x[kPPT][SUBC], best[kPPT];
@@ -289,10 +296,10 @@ assign_kernel(const TP *__restrict__ P, int64_t n, int k, int sub_rt, const doub
                 bi[p] = 0;
             }
             int l = 0;
-            for (; l + 4 <= k; l += 4) {
-                double dl[kPPT][4];
+            for (; l + kU <= k; l += kU) {
+                double dl[kPPT][kU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kU; ++u) {
                     const double *c = Cj + (int64_t)(l + u) * SUBC;
                     double cv[SUBC];
 #pragma unroll
@@ -309,7 +316,7 @@ assign_kernel(const TP *__restrict__ P, int64_t n, int k, int sub_rt, const doub
 #pragma unroll
                 for (int p = 0; p < kPPT; ++p)
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
+                    for (int u = 0; u < kU; ++u)
                         if ((l + u) == 0 || dl[p][u] < best[p]) { best[p] = dl[p][u]; bi[p] = l + u; }
             }
             for (; l < k; ++l) {
