@@ -44,6 +44,9 @@ def parse():
     p.add_argument("--e2e-rows", type=int, default=0,
                    help="rows per rank through the host API (0 = 2M, or the whole config for c5)")
     p.add_argument("--streams", type=int, default=0, help="host pipeline streams (0 = 3, or 6 for c5)")
+    p.add_argument("--train", choices=["auto", "sharded", "rank0"], default="auto",
+                   help="codebook training: row-sharded Lloyd with one all-reduce per iteration (auto: when N > 1), "
+                        "or the fused single-GPU cspq_lloyd_train on rank 0 + broadcast")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -163,7 +166,27 @@ def main():
     # ---- codebooks: GPU Lloyd on rank 0, NCCL broadcast ----
     rm = torch.empty((cfg.m, cfg.k, cfg.sub), dtype=torch.float32, device=dev)
     train_s = None
-    if rank == 0:
+    sharded = args.train == "sharded" or (args.train == "auto" and ws > 1)
+    train_mode = ("sampled codebooks" if cfg.codebook == "sampled" else "fused cspq_lloyd_train") + \
+        (" on rank 0 + NCCL broadcast" if ws > 1 else "")
+    if cfg.codebook == "lloyd" and sharded:
+        # north_star scheme: every rank assigns its row shard of the training sample and one
+        # NCCL all-reduce per iteration combines (counts, sums, objective terms)
+        from paper_2605_25521_b200.distributed import CudaSteps, lloyd_sharded
+        S = C.training_sample(cfg, dev)
+        Ssm = C.subspace_major(S, cfg.m).contiguous()
+        init = torch.from_numpy(C.lloyd_init(cfg, Ssm)).to(dev)
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        res = lloyd_sharded(CudaSteps(Ssm, 0, cfg.n_train, cfg.m, cfg.sub, cfg.k, dev), init,
+                            P.TrainConfig(k=cfg.k, max_iters=cfg.iters, tol=0.0), reduce="allreduce")
+        train_s = time.perf_counter() - t0
+        rm.copy_(torch.from_numpy(np.stack([r.centroids for r in res])))
+        train_mode = (f"row-sharded x{ws}, one NCCL all-reduce per iteration" if ws > 1
+                      else "row-sharded driver at world size 1 (no collective)")
+        del S, Ssm
+    elif rank == 0:
         if cfg.codebook == "sampled":
             Xh = C.generate(cfg, 0, cfg.n, dev).cpu().numpy()
             rm.copy_(torch.from_numpy(C.sampled_codebooks(cfg, Xh)))
@@ -319,7 +342,8 @@ def main():
         enc_s = ms_per_step / 1e3
         train = {"gpu_s": train_s, "subspaces": cfg.m, "iters": cfg.iters, "sample_rows": cfg.n_train,
                  "train_plus_encode_vec_s": rows / (train_s + enc_s),
-                 "def": "wall time of one lloyd_iterate_batched call (all subspaces, fp64, tol=0) incl. the final "
+                 "mode": train_mode,
+                 "def": "wall time of the codebook training (all subspaces, fp64, tol=0) incl. the final "
                         "REFERENCE pass and host transfer of the results"}
         if ws == 1 and not args.no_cpu_baseline:
             from oracle import oracle as O
@@ -348,7 +372,8 @@ def main():
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_desc(cfg, rows, ws, args.scaling), "global_batch": rows * ws,
                        "rows_per_gpu": rows, "parallelism": f"rows sharded x{ws} (codebooks NCCL-broadcast)",
-                       "mode": args.mode, "codebook_train_s": train_s, "l2": l2_note},
+                       "mode": args.mode, "codebook_train_s": train_s, "codebook_training": train_mode,
+                       "l2": l2_note},
             "clocks": clk, "e2e": e2e, "gpu_launches": args.steps, "roofline": roofline, "cpu_baseline": cpu,
             "parity": parity, "flagged_per_subvector": fl.value / max(1, rows * cfg.m * args.steps),
             "step_ms": step_ms,
