@@ -120,3 +120,18 @@ def test_encode_file_dimension_mismatch(P, tmp_path):
     cbs = _codebooks(P, np.random.default_rng(3).standard_normal((2, 256, 2)).astype(np.float32))
     with pytest.raises(P.ConfigError, match="dimensionality 6"):
         P.encode_file(src, cbs, tmp_path / "o.pqcd")
+
+
+def test_encode_file_wide_codes_generic_shape(P, tmp_path):
+    """k = 1000 (uint16 codes, generic kernel) on d_sub = 3 rows: the streamed file equals
+    write_codes(encode_dataset(...)) byte for byte."""
+    rng = np.random.default_rng(21)
+    X = rng.standard_normal((5003, 12)).astype(np.float32)
+    rm = rng.standard_normal((4, 1000, 3)).astype(np.float32)
+    cbs = _codebooks(P, rm)
+    src, out, ref = tmp_path / "w.fvecs", tmp_path / "w.pqcd", tmp_path / "ref.pqcd"
+    P.write_fvecs(src, X)
+    P.encode_file(src, cbs, out, P.ExecutionPlan(batch_rows=1500))
+    P.write_codes(ref, P.encode_dataset(X, cbs))
+    assert out.read_bytes() == ref.read_bytes()
+    assert P.read_codes(out).codes.dtype == np.uint16
