@@ -35,12 +35,14 @@
 //   with sum|x_t c_t| <= ||x|| max_l ||c_l||; a runner-up within 4E (x2
 //   safety) of the best is flagged.
 //
-// Warp roles (256 threads, one CTA per SM, persistent over row groups):
+// Warp roles (64 + 128 kGroups threads, one CTA per SM, persistent over row groups):
 //   warp 0      TMEM allocation + MMA issue (one lane)
-//   warp 1      bulk copies of the prepared codebook image (cp.async.bulk)
-//   warps 2-3   A-operand producers: load rows, split to tf32, write the
-//               K-major no-swizzle core-matrix layout, row norms for the band
-//   warps 4-7   epilogue (TMEM lane quadrant = warp % 4)
+//   warp 1      bulk copies of the prepared codebook image + fp32 codebook (cp.async.bulk)
+//   warps 2..   kGroups epilogue groups of 4 warps (TMEM lane quadrant = warp % 4); item it
+//               belongs to group it % kGroups and TMEM buffer it & 1.  A group drains its
+//               item's accumulator (block + class minima), writes the A operand of its next
+//               item (x prefetched with cp.async, tf32 split), selects the winner and
+//               runner-up, applies the error-band guard and the exact fix-up, stores codes.
 
 #include <cstdlib>
 

@@ -342,6 +342,8 @@ int encode_vecs_file(const char *in_path, int fmt, const char *out_path, const f
         if (tmp_guard) cudaFree(tmp_guard);
     };
     const int64_t br = std::max<int64_t>(1, std::min<int64_t>(batch_rows, std::max<int64_t>(n, 1)));
+    unsigned long long bad[2] = {~0ull, ~0ull};
+    auto run = [&]() -> int {
     for (auto &s : S) {
         CSPQ_CUDA_TRY(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
         CSPQ_CUDA_TRY(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
@@ -358,7 +360,7 @@ int encode_vecs_file(const char *in_path, int fmt, const char *out_path, const f
     const bool needs_guard = variant != CSPQ_VARIANT_REFERENCE && mode != CSPQ_MODE_EXACT;
     if (needs_guard && !guard) {
         CSPQ_CUDA_TRY(cudaMalloc(reinterpret_cast<void **>(&tmp_guard), sizeof(float) * 2 * m));
-        if ((rc = encode_prepare(CB, B, m, k, sub, tmp_guard, S[0].st))) { cleanup(); return rc; }
+        if ((rc = encode_prepare(CB, B, m, k, sub, tmp_guard, S[0].st))) return rc;
         CSPQ_CUDA_TRY(cudaStreamSynchronize(S[0].st));
         guard = tmp_guard;
     }
@@ -396,10 +398,10 @@ int encode_vecs_file(const char *in_path, int fmt, const char *out_path, const f
     // drain in order
     for (int64_t b = std::max<int64_t>(0, nb - (int64_t)S.size()); b < nb && rc == CSPQ_OK; ++b)
         rc = retire(S[b % S.size()]);
-    unsigned long long bad[2] = {~0ull, ~0ull};
-    if (rc == CSPQ_OK) {
-        CSPQ_CUDA_TRY(cudaMemcpy(bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
-    }
+    if (rc == CSPQ_OK) CSPQ_CUDA_TRY(cudaMemcpy(bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
+    return rc;
+    };
+    rc = run();  // every CUDA failure inside returns here, so the resources are always released
     cleanup();
     if (rc) { unlink(out_path); return rc; }
     // the reference walks records in order (io.py:35-62): a bad header or a truncated

@@ -70,6 +70,14 @@ def _check_codes(codes: PQCodes, cbset: CodebookSet):
         raise CorruptionError(f"code out of range for k={cbset.k}")
 
 
+def _codes_array(codes: PQCodes, k: int) -> np.ndarray:
+    """The codes in the width the scoring kernel reads for tables of k entries (uint8 for
+    k <= 256); a code >= k would index past its table (IndexError in the reference)."""
+    if codes.codes.size and int(codes.codes.max()) >= k:
+        raise CorruptionError(f"code out of range for tables of k={k}")
+    return np.ascontiguousarray(codes.codes, dtype=np.uint8 if k <= 256 else np.uint16)
+
+
 def reconstruct_all(codes: PQCodes, codebooks) -> np.ndarray:
     """(n, d) reconstruction of every row (evaluation.py:52-62), gathered on the GPU."""
     cbset = CodebookSet.from_codebooks(codebooks)
@@ -136,7 +144,7 @@ def adc_scores(tables: np.ndarray, codes: PQCodes) -> np.ndarray:
     T = to_device(np.asarray(tables, dtype=np.float32), dev)
     if T.dim() != 2 or T.shape[0] != codes.m:
         raise ConfigError(f"tables shape {tuple(T.shape)} does not match m={codes.m}")
-    c = to_device(codes.codes, dev)
+    c = to_device(_codes_array(codes, T.shape[1]), dev)
     return _scores_dev(T[None], c, T.shape[1], dev)[0].cpu().numpy()
 
 
@@ -160,7 +168,7 @@ def adc_search_batched(queries, codes: PQCodes, codebooks, topn: int):
     topn = min(int(topn), codes.n)
     if codes.n == 0 or topn <= 0:
         return np.empty((Q.shape[0], 0), np.int64), np.empty((Q.shape[0], 0), np.float32)
-    c = to_device(codes.codes, dev)
+    c = to_device(_codes_array(codes, cbset.k), dev)
     Qd = to_device(Q, dev)
     I, D = [], []
     for lo in range(0, Q.shape[0], _Q_CHUNK):
