@@ -194,6 +194,19 @@ struct ItemIter {
         g += stride;
         tn = g < ngroups ? (int)((ntiles - g * kG < kG) ? (ntiles - g * kG) : kG) : 0;
     }
+    // k items ahead (jt counts every pair boundary crossed, as k calls of next() would)
+    __device__ void advance(int k, int64_t stride) {
+        t += k;
+        while (g < ngroups && t >= tn) {
+            t -= tn;
+            ++jt;
+            if (++j >= m) {
+                j = 0;
+                g += stride;
+                tn = g < ngroups ? (int)((ntiles - g * kG < kG) ? (ntiles - g * kG) : kG) : 0;
+            }
+        }
+    }
 };
 
 template <int SUB, typename TIn>
@@ -396,20 +409,23 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             mbar_arrive(&H->b_empty[p & 1]);
         };
 
-        ItemIter ii(blockIdx.x, ngroups, ntiles, m);   // current item
-        ItemIter ic = ii, ip = ii;  // conversion (item + kGroups) / prefetch (item + kGroups kPD)
-        // prologue: stage x for this group's first kPD items, convert its first one
-        uint32_t ipi = 0, ici = 0;
-        for (; ipi < (uint32_t)(kGroups * kPD); ++ipi, ip.next(gridDim.x))
-            if ((int)(ipi % kGroups) == e) prefetch(ip, ipi);
+        // The group walks its own items only (item e, e + kGroups, ...); ic / ip run kGroups
+        // and kGroups kPD items ahead for the A conversion and the x prefetch.
+        ItemIter ii(blockIdx.x, ngroups, ntiles, m);
+        ii.advance(e, gridDim.x);
+        ItemIter ip = ii;
+        uint32_t ipi = e;
+        for (int d = 0; d < kPD; ++d, ipi += kGroups, ip.advance(kGroups, gridDim.x)) prefetch(ip, ipi);
         float norm_cur = 0.f;
-        for (; ici < (uint32_t)kGroups; ++ici, ic.next(gridDim.x))
-            if ((int)ici == e && ic.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(ici); }
-        // ic now points at item kGroups
+        if (ii.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(e); }
+        ItemIter ic = ii;
+        ic.advance(kGroups, gridDim.x);
+        uint32_t ici = e + kGroups;
+        uint32_t rel = 0;  // pairs below rel are released by this thread
 
-        for (uint32_t it = 0; ii.valid(); ++it, ii.next(gridDim.x), ic.next(gridDim.x), ip.next(gridDim.x), ++ici, ++ipi) {
-            if (ii.t == 0 && it > 0) release_pair(ii.jt - 1);  // done with the previous pair's sC
-            if ((int)(it % kGroups) != e) continue;
+        for (uint32_t it = e; ii.valid(); it += kGroups, ii.advance(kGroups, gridDim.x), ic.advance(kGroups, gridDim.x),
+                                          ip.advance(kGroups, gridDim.x), ici += kGroups, ipi += kGroups) {
+            for (; rel < ii.jt; ++rel) release_pair(rel);  // done with those pairs' sC
             const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
             const int j = ii.j;
@@ -545,7 +561,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             }
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 7] = clock64();
         }
-        if (ii.jt > 0) release_pair(ii.jt - 1);  // the last pair
+        for (; rel < ii.jt; ++rel) release_pair(rel);  // ii.jt = every pair this CTA walked
         cp_async_wait<0>();
     }
     tc_fence_before();
