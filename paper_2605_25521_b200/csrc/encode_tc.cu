@@ -56,7 +56,7 @@ namespace {
 
 constexpr int kTM = 128;     // rows per tile (MMA M)
 constexpr int kN = 256;      // centroids (MMA N)
-constexpr int kG = 8;        // tiles per row group (codebook image reuse)
+constexpr int kG = 8;        // max tiles per row group (codebook image reuse); the launch picks 1..kG
 constexpr int kGroups = 3;   // epilogue groups: item it belongs to group it % kGroups
 constexpr int kNA = kGroups; // A-operand stages (a group writes item it + kGroups into item it's stage)
 constexpr int kThreads = 64 + 128 * kGroups;  // MMA warp, loader warp, kGroups x 4 epilogue warps
@@ -178,14 +178,14 @@ struct TcSmemHdr {
 // walk of the (row group, subspace, tile) work items of one CTA
 struct ItemIter {
     int64_t g, ngroups, ntiles;
-    int j, t, m, tn;
+    int j, t, m, tn, gs;  // gs: tiles per row group
     uint32_t jt;  // (row group, subspace) pairs started before the current one
-    __device__ ItemIter(int64_t g0, int64_t ng, int64_t nt, int m_)
-        : g(g0), ngroups(ng), ntiles(nt), j(0), t(0), m(m_), jt(0) {
-        tn = g < ng ? (int)((nt - g * kG < kG) ? (nt - g * kG) : kG) : 0;
+    __device__ ItemIter(int64_t g0, int64_t ng, int64_t nt, int m_, int gs_)
+        : g(g0), ngroups(ng), ntiles(nt), j(0), t(0), m(m_), tn(0), gs(gs_), jt(0) {
+        tn = g < ng ? (int)((nt - g * gs < gs) ? (nt - g * gs) : gs) : 0;
     }
     __device__ bool valid() const { return g < ngroups; }
-    __device__ int64_t tile() const { return g * kG + t; }
+    __device__ int64_t tile() const { return g * gs + t; }
     __device__ void next(int64_t stride) {
         if (++t < tn) return;
         t = 0;
@@ -193,7 +193,7 @@ struct ItemIter {
         if (++j < m) return;
         j = 0;
         g += stride;
-        tn = g < ngroups ? (int)((ntiles - g * kG < kG) ? (ntiles - g * kG) : kG) : 0;
+        tn = g < ngroups ? (int)((ntiles - g * gs < gs) ? (ntiles - g * gs) : gs) : 0;
     }
     // k items ahead (jt counts every pair boundary crossed, as k calls of next() would)
     __device__ void advance(int k, int64_t stride) {
@@ -204,7 +204,7 @@ struct ItemIter {
             if (++j >= m) {
                 j = 0;
                 g += stride;
-                tn = g < ngroups ? (int)((ntiles - g * kG < kG) ? (ntiles - g * kG) : kG) : 0;
+                tn = g < ngroups ? (int)((ntiles - g * gs < gs) ? (ntiles - g * gs) : gs) : 0;
             }
         }
     }
@@ -229,7 +229,7 @@ template <int SUB, typename TIn>
 __global__ void __launch_bounds__(kThreads, 1)
 encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const float *__restrict__ CB,
                  const float *__restrict__ Bv, const float *__restrict__ guard, const uint8_t *__restrict__ img,
-                 uint8_t *__restrict__ codes, int64_t cs, float *__restrict__ best_out, int probe) {
+                 uint8_t *__restrict__ codes, int64_t cs, float *__restrict__ best_out, int gs, int probe) {
     // (a build with the probe / stamp tests folded away measured 7 % slower on c3: its schedule
     // spills at the 128-register cap, so the runtime-uniform tests stay)
     // probe (debug timing only): bit 0 = epilogue skips its min work, bit 1 = no MMAs,
@@ -252,7 +252,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (n + kTM - 1) / kTM;
-    const int64_t ngroups = (ntiles + kG - 1) / kG;
+    const int64_t ngroups = (ntiles + gs - 1) / gs;
 
     for (int i = threadIdx.x; i < 2 * m; i += kThreads) sGuard[i] = guard[i];
     if (threadIdx.x == 0) {
@@ -283,7 +283,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
         if (lane == 0) {
             uint32_t it = 0, jt = 0;
             for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-                const int64_t t0 = g * kG, tn = (ntiles - t0 < kG) ? (ntiles - t0) : kG;
+                const int64_t t0 = g * gs, tn = (ntiles - t0 < gs) ? (ntiles - t0) : gs;
                 for (int j = 0; j < m; ++j, ++jt) {
                     const int jb = jt & 1;
                     mbar_wait(&H->b_full[jb], (jt >> 1) & 1);
@@ -414,7 +414,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
 
         // The group walks its own items only (item e, e + kGroups, ...); ic / ip run kGroups
         // and kGroups kPD items ahead for the A conversion and the x prefetch.
-        ItemIter ii(blockIdx.x, ngroups, ntiles, m);
+        ItemIter ii(blockIdx.x, ngroups, ntiles, m, gs);
         ii.advance(e, gridDim.x);
         ItemIter ip = ii;
         uint32_t ipi = e;
@@ -621,9 +621,20 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, const float *CB, const
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ntiles = (n + kTM - 1) / kTM;
-    const int64_t ngroups = (ntiles + kG - 1) / kG;
+    // tiles per row group: minimise the busiest CTA's cost, tiles x (1 + 0.5 / gs) -- every
+    // (row group, subspace) pair reloads a 41 KB codebook image, measured ~ half a tile's
+    // time spread over the group's tiles (c1's 782 tiles: gs = 6 on all 148 SMs instead of
+    // 8 on 98 SMs; c5: 6; c3: 8)
+    int gs = kG;
+    double busiest = -1.0;
+    for (int g = kG; g >= 1; --g) {
+        const double cost = (double)(((ntiles + g - 1) / g + sms - 1) / sms * g) * (1.0 + 0.5 / g);
+        if (busiest < 0.0 || cost < busiest) { busiest = cost; gs = g; }
+    }
+    if (const char *ge = getenv("CSPQ_TC_GS")) gs = std::max(1, std::min(kG, atoi(ge)));  // debug override
+    const int64_t ngroups = (ntiles + gs - 1) / gs;
     const int grid = (int)std::min<int64_t>(sms, ngroups);
-    kern<<<grid, kThreads, smem, st>>>(X, n, m, xs, CB, B, guard, img, codes, cs, best, probe);
+    kern<<<grid, kThreads, smem, st>>>(X, n, m, xs, CB, B, guard, img, codes, cs, best, gs, probe);
     CSPQ_LAUNCH_CHECK();
     return CSPQ_OK;
 }
