@@ -489,26 +489,25 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
 #pragma unroll
             for (int b = 0; b < 32; ++b) bm[b] = (probe & 1) ? pos_inf_f() : scratch[b * kTM];
             // Final selection on the FMA pipe: ind(x) = sat(1 - (x - m1) * 2^151) is exactly 1
-            // when x == m1 and exactly 0 otherwise (also for NaN/inf), so the winner's index is
-            // sum(ind * i), the number of minima is sum(ind) (a tie -> flag), and the runner-up
-            // is min(x + ind * 3e38).  m1 comes from the class minima (every score is in one).
+            // when x == m1 and exactly 0 otherwise (also for NaN/inf).  Weighted sums give the
+            // winner and detect ties at once: sum(ind * (c + 8)) is in [8, 15] for a unique
+            // minimal class and >= 17 for two or more (likewise blocks with b + 32: [32, 63] vs
+            // >= 65); the runner-up is min(x + ind * 3e38).  m1 comes from the class minima.
             const float m1 = fmin3(fmin3(cls[0], cls[1], cls[2]), fmin3(cls[3], cls[4], cls[5]), fminf(cls[6], cls[7]));
-            float qcf = 0.f, nc = 0.f, wbf = 0.f, nb = 0.f;
+            float qcf = 0.f, wbf = 0.f;
             float oc[8], ob[32];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 const float u = __fmul_rn(__fsub_rn(cls[c], m1), 8.507059e37f);  // 2^126
                 const float ind = __saturatef(__fmaf_rn(u, -33554432.0f, 1.0f)); // 2^25
-                qcf = __fmaf_rn(ind, (float)c, qcf);
-                nc = __fadd_rn(nc, ind);
+                qcf = __fmaf_rn(ind, (float)(c + 8), qcf);
                 oc[c] = __fmaf_rn(ind, 3.0e38f, cls[c]);
             }
 #pragma unroll
             for (int b = 0; b < 32; ++b) {
                 const float u = __fmul_rn(__fsub_rn(bm[b], m1), 8.507059e37f);
                 const float ind = __saturatef(__fmaf_rn(u, -33554432.0f, 1.0f));
-                wbf = __fmaf_rn(ind, (float)b, wbf);
-                nb = __fadd_rn(nb, ind);
+                wbf = __fmaf_rn(ind, (float)(b + 32), wbf);
                 ob[b] = __fmaf_rn(ind, 3.0e38f, bm[b]);
             }
             float sb8[8];
@@ -519,9 +518,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             const float W = sGuard[2 * j] + xnorm * sGuard[2 * j + 1];
             const float thr = m1 + 4.0f * kE * W + 1e-36f;
             const int64_t row = ii.tile() * kTM + r;
-            int code = 8 * __float2int_rz(wbf) + __float2int_rz(qcf);
-            const bool flag = (row < n) && (!(m1 < pos_inf_f()) || !(thr < pos_inf_f()) || nb != 1.0f || nc != 1.0f ||
-                                            second <= thr);
+            int code = 8 * (__float2int_rz(wbf) - 32) + (__float2int_rz(qcf) - 8);
+            const bool unique = qcf >= 8.0f && qcf < 16.0f && wbf >= 32.0f && wbf < 64.0f;
+            const bool flag = (row < n) && (!(m1 < pos_inf_f()) || !(thr < pos_inf_f()) || !unique || second <= thr);
             // exact warp-cooperative re-encode of flagged rows (x and the fp32 codebook from
             // shared memory: the item's x slot stays valid until kPD more owned items)
             unsigned mask = __ballot_sync(0xffffffffu, flag && !(probe & 15));
