@@ -72,8 +72,11 @@ def oracle_codebooks(cfg, dev):
     (no GPU compute -- only the seeded data generator)."""
     import numpy as np
     from paper_2605_25521_b200 import configs as C
-    S = C.training_sample(cfg, dev)
-    rm = np.ascontiguousarray(C.lloyd_init(cfg, C.subspace_major(S, cfg.m)).astype(np.float32))
+    if cfg.codebook == "sampled":  # c1: distinct data subvectors, as the B200 arm uses
+        rm = np.ascontiguousarray(C.sampled_codebooks(cfg, C.generate(cfg, 0, cfg.n, dev).cpu().numpy()))
+    else:
+        S = C.training_sample(cfg, dev)
+        rm = np.ascontiguousarray(C.lloyd_init(cfg, C.subspace_major(S, cfg.m)).astype(np.float32))
     from oracle.oracle import compute_biases
     return rm, compute_biases(rm)
 
