@@ -112,3 +112,30 @@ def test_tensor_error_within_band(P, oracle):
         W = bmax[None, :] + nrm * cmax[None, :]
         err = np.abs(best.astype(np.float64) - wbest.astype(np.float64))[same] / W[same]
         assert err.max() < 2.2e-6 / 4, f"scale {scale}: observed {err.max():.3e} vs bound 2.2e-6"
+
+
+@pytest.mark.parametrize("sub,m", [(8, 4), (4, 6)])
+def test_nonfinite_and_extreme_rows_tensor(P, oracle, sub, m):
+    """NaN in one or all dimensions, +-inf, values whose scores overflow, subnormals and
+    zero rows: every such row must be caught by the guard and re-encoded exactly (the
+    oracle: NaN never wins, an all-NaN row gets code 0)."""
+    rng = np.random.default_rng(sub * 100 + m)
+    n = 4096
+    X = rng.standard_normal((n, m * sub)).astype(np.float32)
+    sel = rng.choice(n, 1200, replace=False)
+    kinds = np.array_split(sel, 8)
+    X[kinds[0], rng.integers(0, m * sub, kinds[0].size)] = np.nan
+    X[kinds[1]] = np.nan
+    X[kinds[2], rng.integers(0, m * sub, kinds[2].size)] = np.inf
+    X[kinds[3], rng.integers(0, m * sub, kinds[3].size)] = -np.inf
+    X[kinds[4]] *= np.float32(1e30)
+    X[kinds[5]] = (rng.standard_normal((kinds[5].size, m * sub)) * 1e-40).astype(np.float32)
+    X[kinds[6]] = 0.0
+    X[kinds[7], rng.integers(0, m * sub, kinds[7].size)] = np.float32(3e38)
+    rm = rng.standard_normal((m, 256, sub)).astype(np.float32)
+    rm[:, 7] = 0.0                      # a zero centroid: exact-zero scores for the zero rows
+    rm[:, 9] = rm[:, 8]                 # an exact duplicate: ties everywhere it wins
+    cs = cset_of(P, rm)
+    want = oracle.encode(X, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM)
+    got = tc_codes(P, X, cs)
+    assert got.tobytes() == want.tobytes(), int((got != want).sum())
