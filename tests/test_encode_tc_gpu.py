@@ -139,3 +139,18 @@ def test_nonfinite_and_extreme_rows_tensor(P, oracle, sub, m):
     want = oracle.encode(X, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM)
     got = tc_codes(P, X, cs)
     assert got.tobytes() == want.tobytes(), int((got != want).sum())
+
+
+@pytest.mark.parametrize("offset", [1e3, 3e4])
+def test_large_common_offset_tensor(P, oracle, offset):
+    """Vectors and centroids around a large common offset: b and x.c are huge and cancel,
+    so the tensor-core error is largest relative to the score gaps.  The band must still
+    catch every near-tie (codes equal the oracle's; more rows take the exact fix-up)."""
+    rng = np.random.default_rng(int(offset))
+    m, sub, n = 4, 8, 20_000
+    X = (offset + rng.standard_normal((n, m * sub))).astype(np.float32)
+    rm = (offset + rng.standard_normal((m, 256, sub))).astype(np.float32)
+    cs = cset_of(P, rm)
+    want = oracle.encode(X, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM)
+    got = tc_codes(P, X, cs)
+    assert got.tobytes() == want.tobytes(), int((got != want).sum())
