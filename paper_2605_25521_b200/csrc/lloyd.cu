@@ -753,7 +753,10 @@ int lloyd_assign(const void *P, int pf64, int64_t n, int m, int sub, int k, cons
     const size_t need = (size_t)k * (sub + 1) * sizeof(double);
     const int use_smem = need <= 96 * 1024;
     const size_t smem = use_smem ? need : 0;
-    dim3 grid((unsigned)grid_for(e - b, 256, 148 * 8), (unsigned)m);
+    // the fixed-sub kernels take CSPQ_LLOYD_PPT points per thread: size the grid for that, or
+    // most CTAs would only stage the codebook and exit
+    const int64_t per_thread = (sub == 8 || sub == 4) ? CSPQ_LLOYD_PPT : 1;
+    dim3 grid((unsigned)grid_for((e - b + per_thread - 1) / per_thread, 256, 148 * 8), (unsigned)m);
     CSPQ_TP_DISPATCH(pf64, P, {
         if (sub == 8) {
             CSPQ_CUDA_TRY(cudaFuncSetAttribute(assign_kernel<8, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
