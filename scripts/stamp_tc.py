@@ -17,7 +17,7 @@ for _ in range(2):
     P.encode_dataset_device(X, cs, P.ExecutionPlan(mode="tensor"), best=best)
 torch.cuda.synchronize()
 st = best.view(torch.int64).flatten()[:2048 * 8].cpu().numpy().reshape(2048, 8).astype(np.float64)
-names = ["mma_afull", "mma_tempty", "mma_commit", "prod_cpwait", "prod_aempty", "epi_tfull", "epi_release", "epi_done"]
+names = ["mma_afull", "mma_tempty", "mma_commit", "unused3", "unused4", "epi_tfull", "epi_release", "epi_done"]
 base = st[0, 0]
 st = st - base
 for i in list(range(0, 12)) + list(range(1000, 1012)):
