@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--e2e-rows", type=int, default=0,
                    help="rows per rank through the host API (0 = 2M, or the whole config for c5)")
     p.add_argument("--streams", type=int, default=0, help="host pipeline streams (0 = 3, or 6 for c5)")
+    p.add_argument("--e2e-batch", type=int, default=0, help="host pipeline batch rows (0 = 131072, or 4096 for c5)")
     p.add_argument("--train", choices=["auto", "sharded", "rank0"], default="auto",
                    help="codebook training: row-sharded Lloyd with one all-reduce per iteration (auto: when N > 1), "
                         "or the fused single-GPU cspq_lloyd_train on rank 0 + broadcast")
@@ -266,7 +267,7 @@ def main():
         # c5 is the streaming config: the reference's 4096-row batches from pinned host memory,
         # whole dataset per step, with per-batch H2D -> encode -> D2H latency from device events
         ne = min(args.e2e_rows or (cfg.n if cfg.batch else 2_000_000), rows)
-        batch_rows = cfg.batch or (1 << 18)
+        batch_rows = cfg.batch or args.e2e_batch or (1 << 17)  # 128K..1M rows all saturate PCIe (54-55 GB/s)
         Xh = P.pinned_empty((ne, cfg.d), np.uint8 if cfg.dtype == "u8" else np.float32)
         Xh[:] = X[:ne].cpu().numpy()
         codes_h = P.pinned_empty((ne, cfg.m), np.uint8)
