@@ -201,6 +201,8 @@ def encode_dataset_device(X, codebooks, plan: ExecutionPlan | None = None, *,
     t = torch()
     plan = plan or ExecutionPlan()
     cbset = CodebookSet.from_codebooks(codebooks)
+    if not (isinstance(X, t.Tensor) and X.is_cuda):
+        raise ConfigError("encode_dataset_device needs a CUDA tensor (use encode_dataset for host arrays)")
     if X.dim() != 2:
         raise ConfigError(f"dataset must be 2-D, got shape {tuple(X.shape)}")
     if X.dtype not in (t.float32, t.uint8):
@@ -212,6 +214,12 @@ def encode_dataset_device(X, codebooks, plan: ExecutionPlan | None = None, *,
     cdt = t.uint8 if cbset.k <= 256 else t.int16
     if out is None:
         out = t.empty((n, cbset.m), dtype=cdt, device=dev)
+    elif (not isinstance(out, t.Tensor) or out.device != dev or out.dtype != cdt or tuple(out.shape) != (n, cbset.m)
+          or out.stride(1) != 1):
+        raise ConfigError(f"out must be a ({n}, {cbset.m}) {cdt} tensor on {dev} with unit column stride")
+    if best is not None and (not isinstance(best, t.Tensor) or best.device != dev or best.dtype != t.float32
+                             or tuple(best.shape) != (n, cbset.m) or not best.is_contiguous()):
+        raise ConfigError(f"best must be a contiguous ({n}, {cbset.m}) float32 tensor on {dev}")
     if n == 0:
         return out
     if d != cbset.d:
@@ -223,6 +231,8 @@ def encode_dataset_device(X, codebooks, plan: ExecutionPlan | None = None, *,
     if mode == "tensor" and not use_tc:
         raise ConfigError("mode='tensor' needs k=256, sub_dim in {4, 8}, a REFORMULATED/BLOCKED variant "
                           "and 16-byte aligned rows")
+    if best is not None and not use_tc:
+        raise ConfigError("best (winning tensor-core scores) is only produced by the tensor-core path")
     with t.cuda.device(dev):
         if use_tc:
             img = cbset.tc_image(dev, nobias=not precomputed_bias and plan.variant is EncoderVariant.BLOCKED)

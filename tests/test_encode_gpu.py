@@ -320,3 +320,22 @@ def test_full_size_properties_c3_slice(P, oracle):
     idx = np.sort(rng.choice(n, 20_000, replace=False))
     sel = X[torch.from_numpy(idx).to(dev)].cpu().numpy()
     assert full[torch.from_numpy(idx).to(dev)].cpu().numpy().tobytes() == _oracle_codes(oracle, sel, cs).tobytes()
+
+
+def test_device_output_validation(P):
+    import torch
+    rng = np.random.default_rng(3)
+    rm = rng.standard_normal((2, 256, 4)).astype(np.float32)
+    cbs = [P.Codebook.from_rowmajor(j, rm[j]) for j in range(2)]
+    X = torch.from_numpy(rng.standard_normal((10, 8)).astype(np.float32)).cuda()
+    with pytest.raises(P.ConfigError, match="out must be"):
+        P.encode_dataset_device(X, cbs, out=torch.empty((10, 3), dtype=torch.uint8, device="cuda"))
+    with pytest.raises(P.ConfigError, match="out must be"):
+        P.encode_dataset_device(X, cbs, out=torch.empty((10, 2), dtype=torch.int32, device="cuda"))
+    with pytest.raises(P.ConfigError, match="best must be"):
+        P.encode_dataset_device(X, cbs, best=torch.empty((10, 2), dtype=torch.float64, device="cuda"))
+    with pytest.raises(P.ConfigError, match="only produced by the tensor-core path"):
+        P.encode_dataset_device(X, cbs, P.ExecutionPlan(mode="exact"),
+                                best=torch.empty((10, 2), dtype=torch.float32, device="cuda"))
+    out = torch.empty((10, 2), dtype=torch.uint8, device="cuda")
+    assert P.encode_dataset_device(X, cbs, out=out) is out

@@ -158,3 +158,15 @@ def test_configs_host_definitions():
     idx = C.sample_indices(c3.scaled(n=10_000, n_train=500))
     assert idx.shape == (500,) and np.all(np.diff(idx) > 0)
     assert np.array_equal(idx, C.sample_indices(c3.scaled(n=10_000, n_train=500)))
+
+
+def test_encode_dataset_device_rejects_host_tensors_and_bad_outputs():
+    """Argument checks that run before any CUDA call (no GPU needed)."""
+    import torch
+    import paper_2605_25521_b200 as P
+    rm = np.random.default_rng(0).standard_normal((2, 256, 4)).astype(np.float32)
+    cbs = [P.Codebook.from_rowmajor(j, rm[j]) for j in range(2)]
+    with pytest.raises(P.ConfigError, match="CUDA tensor"):
+        P.encode_dataset_device(torch.zeros((4, 8)), cbs)
+    with pytest.raises(P.ConfigError, match="CUDA tensor"):
+        P.encode_dataset_device(np.zeros((4, 8), np.float32), cbs)
