@@ -102,7 +102,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
                      : "=r"(done) : "r"(smem_u32(bar)), "r"(parity), "r"(kSuspendNs) : "memory");
         if (done) return;
         if (first) t0 = clock64();  // (the clock is read only once a wait actually waits)
-        else if (clock64() - t0 > 4000000000ll) __trap();  // ~2 s of waiting: a lost arrival
+        else if (clock64() - t0 > 20000000000ll) __trap();  // ~10 s: a lost arrival (not a time slice)
     }
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
