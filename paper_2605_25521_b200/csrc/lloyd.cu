@@ -666,19 +666,49 @@ __global__ void kpp_div_kernel(const double *__restrict__ d2, int64_t n, const d
 }
 
 // rng.choice(n, p=p): cdf = cumsum(p) (sequential); cdf /= cdf[-1];
-// idx = searchsorted(cdf, u, 'right').  One thread per subspace runs the
-// chain in place, then binary-searches the normalised (monotone) cdf.
-__global__ void kpp_choose_kernel(double *__restrict__ pp, int64_t n, int m, int k, int c,
-                                  const double *__restrict__ total, const double *__restrict__ u,
-                                  int32_t *__restrict__ status, const void *P, int pf64, int sub,
-                                  double *__restrict__ C64) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= m || status[j]) return;
-    if (!(total[j] > 0.0)) { status[j] = 2; return; }  // all mass on chosen points
+// idx = searchsorted(cdf, u, 'right').  One CTA per subspace: chunks of the
+// probabilities are staged in shared memory with coalesced loads, thread 0
+// runs numpy's sequential chain over the chunk (in shared memory, loads issued
+// ahead of the dependent adds), the CTA writes the chunk back; then a binary
+// search over the normalised (monotone) cdf.
+constexpr int kKppChunk = 4096;
+__global__ void __launch_bounds__(256) kpp_choose_kernel(double *__restrict__ pp, int64_t n, int m, int k, int c,
+                                                         const double *__restrict__ total, const double *__restrict__ u,
+                                                         int32_t *__restrict__ status, const void *P, int pf64, int sub,
+                                                         double *__restrict__ C64) {
+    __shared__ double buf[kKppChunk];
+    __shared__ double s_run;
+    const int j = blockIdx.x;
+    if (status[j]) return;
+    if (!(total[j] > 0.0)) {  // all mass on chosen points
+        if (threadIdx.x == 0) status[j] = 2;
+        return;
+    }
     double *cdf = pp + (int64_t)j * n;
-    double run = 0.0;
-    for (int64_t i = 0; i < n; ++i) { run = __dadd_rn(run, cdf[i]); cdf[i] = run; }
-    const double last = run;
+    if (threadIdx.x == 0) s_run = 0.0;
+    for (int64_t c0 = 0; c0 < n; c0 += kKppChunk) {
+        const int len = (int)(n - c0 < kKppChunk ? n - c0 : kKppChunk);
+        for (int i = threadIdx.x; i < len; i += blockDim.x) buf[i] = cdf[c0 + i];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double run = s_run;
+            int i = 0;
+            for (; i + 8 <= len; i += 8) {
+                double v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = buf[i + q];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) { run = __dadd_rn(run, v[q]); buf[i + q] = run; }
+            }
+            for (; i < len; ++i) { run = __dadd_rn(run, buf[i]); buf[i] = run; }
+            s_run = run;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < len; i += blockDim.x) cdf[c0 + i] = buf[i];
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    const double last = s_run;
     const double uu = u[(int64_t)j * (k - 1) + (c - 1)];
     int64_t lo = 0, hi = n;  // first i with cdf[i]/last > uu
     while (lo < hi) {
@@ -906,7 +936,7 @@ int kmeanspp(const void *P, int pf64, int64_t n, int m, int sub, int k, const in
             if ((rc = pairwise_obj(d2, n, 0, n, m, nullptr, ws, L, total, st))) return rc;
             kpp_div_kernel<<<g, 256, 0, st>>>(d2, n, total, status, pp);
             CSPQ_LAUNCH_CHECK();
-            kpp_choose_kernel<<<(m + 31) / 32, 32, 0, st>>>(pp, n, m, k, c, total, u, status, P, pf64, sub, C64);
+            kpp_choose_kernel<<<m, 256, 0, st>>>(pp, n, m, k, c, total, u, status, P, pf64, sub, C64);
             CSPQ_LAUNCH_CHECK();
             kpp_dist_kernel<TP><<<g, 256, 0, st>>>(Pt, n, sub, C64, k, c, status, d2, 0);
             CSPQ_LAUNCH_CHECK();

@@ -135,17 +135,23 @@ def lloyd_iterate(pts64: np.ndarray, centroids: np.ndarray, cfg: TrainConfig) ->
 def kmeanspp_init_batched(points_list, k: int, rngs, dev=None) -> np.ndarray:
     """training.py:76-92 for m subspaces: the host draws exactly what the
     reference draws from each generator (rng.integers(n), then one
-    rng.random() per rng.choice), the GPU does the D^2 arithmetic."""
+    rng.random() per rng.choice), the GPU does the D^2 arithmetic.
+    points_list: [(n, sub)] arrays, or an already stacked (m, n, sub) CUDA
+    tensor (float32 or float64)."""
     N.require_cuda()
     t = torch()
-    P, pf64 = _stack_points(points_list)
+    if isinstance(points_list, t.Tensor):
+        P = points_list.contiguous()
+        pf64 = 1 if P.dtype == t.float64 else 0
+    else:
+        P, pf64 = _stack_points(points_list)
     m, n, sub = P.shape
     first = np.array([int(r.integers(n)) for r in rngs], dtype=np.int64)
     u = np.stack([r.random(k - 1) if k > 1 else np.zeros(0) for r in rngs]).astype(np.float64)
     u = np.ascontiguousarray(u.reshape(m, max(k - 1, 0)))
     dev = device() if dev is None else dev
     with t.cuda.device(dev):
-        Pd = to_device(P, dev)
+        Pd = P if isinstance(P, t.Tensor) and P.device == dev else to_device(P, dev)
         fd = to_device(first, dev)
         ud = to_device(u if u.size else np.zeros((m, 1)), dev)
         C = t.zeros((m, k, sub), dtype=t.float64, device=dev)
@@ -161,11 +167,25 @@ def kmeanspp_init_batched(points_list, k: int, rngs, dev=None) -> np.ndarray:
     return Ch
 
 
+def _distinct_at_least(pts64: np.ndarray, k: int) -> bool:
+    """np.unique(pts64, axis=0).shape[0] >= k (training.py:102-105) without sorting every
+    row: rows go into a set until it holds k of them (a few hundred rows on real data).
+    Adding 0.0 maps -0.0 to +0.0 so the bytes compare like np.unique's values do."""
+    a = np.ascontiguousarray(pts64 + 0.0)
+    rows = a.view(np.dtype((np.void, a.dtype.itemsize * a.shape[1]))).ravel()
+    seen = set()
+    for lo in range(0, rows.shape[0], 1024):
+        seen.update(rows[lo:lo + 1024].tolist())
+        if len(seen) >= k:
+            return True
+    return False
+
+
 def _validate_points(pts64: np.ndarray, k: int):
     n = pts64.shape[0]
     if n < k:
         raise TrainingError(f"need at least k={k} training points, got {n}")
-    if k > 1 and np.unique(pts64, axis=0).shape[0] < k:
+    if k > 1 and not _distinct_at_least(pts64, k):
         raise TrainingError(f"degenerate data: fewer than k={k} distinct training points")
 
 
@@ -202,8 +222,12 @@ def _train_many(subspace_points, cfg: TrainConfig, rngs, labels):
         except (TrainingError, DataError) as exc:
             raise type(exc)(f"subspace {j}: {exc}") from None
         sampled.append(s64)
-    init = kmeanspp_init_batched(sampled, cfg.k, rngs)
-    return lloyd_iterate_batched(sampled, init, cfg)
+    # stack (and exactness-check) once, move to the GPU once; both stages read the tensor
+    P, _ = _stack_points(sampled)
+    dev = device()
+    Pd = to_device(P, dev)
+    init = kmeanspp_init_batched(Pd, cfg.k, rngs, dev)
+    return lloyd_iterate_batched(Pd, init, cfg, dev)
 
 
 def train_codebook(subvectors: np.ndarray, cfg: TrainConfig, subspace_index: int = 0) -> Codebook:
@@ -242,6 +266,8 @@ def train_all_codebooks_report(dataset, params, cfg: TrainConfig):
         raise TrainingError(f"dataset dimensionality {data.shape[1]} does not match d={params.d}")
     rngs = _subspace_rngs(cfg.seed, params.m)
     sub = params.sub_dim
-    pts = [np.ascontiguousarray(data[:, j * sub:(j + 1) * sub]) for j in range(params.m)]
+    # column views: _sample gathers only the sampled rows (the same arrays the reference's
+    # per-subspace slice + sample produce, without copying every column block first)
+    pts = [data[:, j * sub:(j + 1) * sub] for j in range(params.m)]
     reports = _train_many(pts, cfg, rngs, range(params.m))
     return [Codebook.from_rowmajor(j, r.centroids) for j, r in enumerate(reports)], reports
