@@ -88,7 +88,7 @@ bool is_pinned(const void *p) {
 
 void par_memcpy(void *dst, const void *src, size_t bytes) {
     const size_t kMin = 8u << 20;
-    const unsigned nt = std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency()));
+    const unsigned nt = std::min<unsigned>(32u, std::max(1u, std::thread::hardware_concurrency()));
     if (bytes < kMin || nt == 1) {
         std::memcpy(dst, src, bytes);
         return;
