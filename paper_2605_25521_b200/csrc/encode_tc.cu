@@ -66,6 +66,8 @@ constexpr int kNC = 1;        // accumulator chunks per item (N = 256 / kNC per 
 constexpr int kCW = 256 / kNC;  // chunk width in TMEM columns (a multiple of 64: one tcgen05.ld x64)
 constexpr int kPD = 2;        // cp.async prefetch distance, in the group's own items
 constexpr int kRing = 3;      // x slots per group (> kPD: an item's slot outlives its fix-up)
+constexpr int kScrW = 36;     // floats per row of the block-minima scratch: 32 + 4 pad, so the 16-B
+                              // stores / loads of 8 consecutive rows hit 8 distinct bank quads
 
 template <int SUB>
 struct TcShape {
@@ -92,9 +94,18 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 }
 // bounded wait: a lost arrival traps (error) instead of hanging the device
 constexpr uint32_t kSuspendNs = 1000000;
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, bool spin = false) {
     uint32_t done = 0;
     long long t0 = 0;
+    if (spin) {  // (experiment) poll without suspending
+        for (long long i = 0;; ++i) {
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                         : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+            if (done) return;
+            if (i == 0) t0 = clock64();
+            else if ((i & 1023) == 0 && clock64() - t0 > 20000000000ll) __trap();
+        }
+    }
     for (bool first = true;; first = false) {
         // suspend (woken by the phase flip) instead of busy polling: spinning warps steal
         // issue slots from the epilogue warps that share their SM sub-partition
@@ -219,8 +230,8 @@ struct TcSmem {
     static constexpr size_t oA = oB + 2 * (size_t)S::kBBytes;
     static constexpr size_t oC = oA + kNA * (size_t)S::kABytes;
     static constexpr size_t oX = oC + 2 * (size_t)kCFloats * 4;
-    static constexpr size_t oS = oX + kGroups * kRing * (size_t)kXBytes;  // block-minima scratch [kGroups][32][kTM]
-    static constexpr size_t oG = oS + (size_t)kGroups * 32 * kTM * 4;        // guard constants (2 m floats)
+    static constexpr size_t oS = oX + kGroups * kRing * (size_t)kXBytes;  // block-minima scratch [kGroups][kTM][kScrW]
+    static constexpr size_t oG = oS + (size_t)kGroups * kTM * kScrW * 4;     // guard constants (2 m floats)
     static size_t total(int m) { return oG + ((size_t)2 * m * 4 + 15) / 16 * 16 + sizeof(TcSmemHdr) + 16; }
 };
 
@@ -286,15 +297,15 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                 const int64_t t0 = g * gs, tn = (ntiles - t0 < gs) ? (ntiles - t0) : gs;
                 for (int j = 0; j < m; ++j, ++jt) {
                     const int jb = jt & 1;
-                    mbar_wait(&H->b_full[jb], (jt >> 1) & 1);
+                    mbar_wait(&H->b_full[jb], (jt >> 1) & 1, probe & 256);
                     for (int t = 0; t < tn; ++t, ++it) {
                         const int as = it % kNA, tb = it & 1;
-                        mbar_wait(&H->a_full[as], (it / kNA) & 1);
+                        mbar_wait(&H->a_full[as], (it / kNA) & 1, probe & 256);
                         if (stamp && it < kStampItems) stamp[it * 8 + 0] = clock64();
                         const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
                         for (int c = 0; c < kNC; ++c) {
                             // chunk c of buffer tb drained by the scan of item it - 2
-                            if (it >= 2) mbar_wait(&H->t_empty[(it - 2) & 3][c], ((it - 2) >> 2) & 1);
+                            if (it >= 2) mbar_wait(&H->t_empty[(it - 2) & 3][c], ((it - 2) >> 2) & 1, probe & 256);
                             if (stamp && c == 0 && it < kStampItems) stamp[it * 8 + 1] = clock64();
                             tc_fence_after();
                             const uint32_t bc = b0 + (uint32_t)(c * (kCW / 8) * S::kRowGroupBytes);  // centroids c kCW ..
@@ -319,7 +330,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
                 for (int j = 0; j < m; ++j, ++jt) {
                     const int jb = jt & 1;
-                    mbar_wait(&H->b_empty[jb], ((jt >> 1) & 1) ^ 1);
+                    mbar_wait(&H->b_empty[jb], ((jt >> 1) & 1) ^ 1, probe & 1024);
                     mbar_arrive_expect_tx(&H->b_full[jb], S::kBBytes + L::kCFloats * 4);
                     bulk_g2s(sB + jb * S::kBBytes, img + (int64_t)j * S::kBBytes, S::kBBytes, &H->b_full[jb]);
                     float *cdst = sC + jb * L::kCFloats;
@@ -337,7 +348,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
         const int e = (warp - 2) >> 2;  // group: items it with it % kGroups == e
         const int q = warp & 3;
         const int r = 32 * q + lane;
-        float *scratch = sScr + (size_t)e * 32 * kTM + r;  // this thread's block minima, [32][kTM]
+        float *scratch = sScr + ((size_t)e * kTM + r) * kScrW;  // this thread's 32 block minima
         constexpr float kE = (float)((4.0 / 4194304.0 + S::kSteps / 4194304.0 * (1.0 + 1.0 / 1024.0) + (SUB + 1) / 16777216.0) * 1.01);
         auto ring = [&](uint32_t item) -> unsigned char * {  // x slot of one of the group's items
             return sX + ((size_t)e * kRing + (item / kGroups) % kRing) * L::kXBytes + r * SUB * sizeof(TIn);
@@ -440,7 +451,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                 constexpr int kLdPerChunk = kCW / 64;
                 const int c = ch / kLdPerChunk;
                 if (ch % kLdPerChunk == 0) {
-                    mbar_wait(&H->t_full[it & 3][c], (it >> 2) & 1);
+                    mbar_wait(&H->t_full[it & 3][c], (it >> 2) & 1, probe & 512);
                     if (stamp && r == 0 && ch == 0 && it < kStampItems) stamp[it * 8 + 5] = clock64();
                     tc_fence_after();
                 }
@@ -455,6 +466,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                     cls[ch] = __fadd_rn(SV(0), SV(63));
                     continue;
                 }
+                float bmc[8];
 #pragma unroll
                 for (int bp = 0; bp < 4; ++bp) {
 #pragma unroll
@@ -462,10 +474,12 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         const int o = 16 * bp + 8 * hh;
-                        scratch[(8 * ch + 2 * bp + hh) * kTM] = fmin3(fmin3(SV(o), SV(o + 1), SV(o + 2)),
-                                                                     fmin3(SV(o + 3), SV(o + 4), SV(o + 5)), fminf(SV(o + 6), SV(o + 7)));
+                        bmc[2 * bp + hh] = fmin3(fmin3(SV(o), SV(o + 1), SV(o + 2)), fmin3(SV(o + 3), SV(o + 4), SV(o + 5)),
+                                                 fminf(SV(o + 6), SV(o + 7)));
                     }
                 }
+                reinterpret_cast<float4 *>(scratch + 8 * ch)[0] = make_float4(bmc[0], bmc[1], bmc[2], bmc[3]);
+                reinterpret_cast<float4 *>(scratch + 8 * ch)[1] = make_float4(bmc[4], bmc[5], bmc[6], bmc[7]);
 #undef SV
             }
             if (probe & 1) {  // (timing probe: no TMEM reads; still walk the barriers)
@@ -485,42 +499,47 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             }
             const float xnorm = norm_cur;
             norm_cur = norm_next;
+            if (probe & 128) {  // (timing probe: no selection / fix-up; garbage codes)
+                const int64_t row = ii.tile() * kTM + r;
+                if (row < n && !(probe & 64)) codes[row * cs + j] = (uint8_t)(__float_as_uint(cls[0] + xnorm) & 255);
+                continue;
+            }
             float bm[32];
 #pragma unroll
-            for (int b = 0; b < 32; ++b) bm[b] = (probe & 1) ? pos_inf_f() : scratch[b * kTM];
-            // Final selection on the FMA pipe: ind(x) = sat(1 - (x - m1) * 2^151) is exactly 1
-            // when x == m1 and exactly 0 otherwise (also for NaN/inf).  Weighted sums give the
-            // winner and detect ties at once: sum(ind * (c + 8)) is in [8, 15] for a unique
-            // minimal class and >= 17 for two or more (likewise blocks with b + 32: [32, 63] vs
-            // >= 65); the runner-up is min(x + ind * 3e38).  m1 comes from the class minima.
+            for (int b4 = 0; b4 < 8; ++b4) {
+                const float4 t4 = reinterpret_cast<const float4 *>(scratch)[b4];
+                bm[4 * b4] = t4.x; bm[4 * b4 + 1] = t4.y; bm[4 * b4 + 2] = t4.z; bm[4 * b4 + 3] = t4.w;
+            }
+            // Final selection on the FMA pipe.  m1 = the minimum (of the class minima); the band
+            // indicator ind(v) = sat(1 - (v - m1) / (4 E W)) is exactly 1 for v == m1, exactly 0
+            // beyond the guard band and in between inside it (0 for NaN).  A (row, subspace) is
+            // decided iff exactly one class minimum and exactly one block minimum have a nonzero
+            // indicator (the sums of the indicators are exactly 1): then no other centroid lies
+            // within the band -- any other centroid shares neither its block nor its class with
+            // the winner, or only one of them, and its block or class minimum would be in the band
+            // -- and the indicator-weighted index sums give the winner's block and class exactly.
+            // (An indicator < 2^-24 can vanish in a sum; its value is > 3.9 E W from m1, outside
+            // the 2 E W that exactness needs.)
             const float m1 = fmin3(fmin3(cls[0], cls[1], cls[2]), fmin3(cls[3], cls[4], cls[5]), fminf(cls[6], cls[7]));
-            float qcf = 0.f, wbf = 0.f;
-            float oc[8], ob[32];
+            const float W = sGuard[2 * j] + xnorm * sGuard[2 * j + 1];
+            float kinv;
+            asm("rcp.approx.f32 %0, %1;" : "=f"(kinv) : "f"(4.0f * kE * W));  // inf for W = 0: every ind = 0 (flag)
+            float qcf = 0.f, ncf = 0.f, wbf = 0.f, nbf = 0.f;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                const float u = __fmul_rn(__fsub_rn(cls[c], m1), 8.507059e37f);  // 2^126
-                const float ind = __saturatef(__fmaf_rn(u, -33554432.0f, 1.0f)); // 2^25
+                const float ind = __saturatef(__fmaf_rn(__fsub_rn(cls[c], m1), -kinv, 1.0f));
                 qcf = __fmaf_rn(ind, (float)(c + 8), qcf);
-                oc[c] = __fmaf_rn(ind, 3.0e38f, cls[c]);
+                ncf = __fadd_rn(ncf, ind);
             }
 #pragma unroll
             for (int b = 0; b < 32; ++b) {
-                const float u = __fmul_rn(__fsub_rn(bm[b], m1), 8.507059e37f);
-                const float ind = __saturatef(__fmaf_rn(u, -33554432.0f, 1.0f));
+                const float ind = __saturatef(__fmaf_rn(__fsub_rn(bm[b], m1), -kinv, 1.0f));
                 wbf = __fmaf_rn(ind, (float)(b + 32), wbf);
-                ob[b] = __fmaf_rn(ind, 3.0e38f, bm[b]);
+                nbf = __fadd_rn(nbf, ind);
             }
-            float sb8[8];
-#pragma unroll
-            for (int g8 = 0; g8 < 8; ++g8) sb8[g8] = fminf(fmin3(ob[4 * g8], ob[4 * g8 + 1], ob[4 * g8 + 2]), ob[4 * g8 + 3]);
-            const float second = fmin3(fmin3(fmin3(sb8[0], sb8[1], sb8[2]), fmin3(sb8[3], sb8[4], sb8[5]), fminf(sb8[6], sb8[7])),
-                                       fmin3(oc[0], oc[1], oc[2]), fmin3(fmin3(oc[3], oc[4], oc[5]), oc[6], oc[7]));
-            const float W = sGuard[2 * j] + xnorm * sGuard[2 * j + 1];
-            const float thr = m1 + 4.0f * kE * W + 1e-36f;
             const int64_t row = ii.tile() * kTM + r;
             int code = 8 * (__float2int_rz(wbf) - 32) + (__float2int_rz(qcf) - 8);
-            const bool unique = qcf >= 8.0f && qcf < 16.0f && wbf >= 32.0f && wbf < 64.0f;
-            const bool flag = (row < n) && (!(m1 < pos_inf_f()) || !(thr < pos_inf_f()) || !unique || second <= thr);
+            const bool flag = (row < n) && !(ncf == 1.0f && nbf == 1.0f);
             // exact warp-cooperative re-encode of flagged rows (x and the fp32 codebook from
             // shared memory: the item's x slot stays valid until kPD more owned items)
             unsigned mask = __ballot_sync(0xffffffffu, flag && !(probe & 15));
