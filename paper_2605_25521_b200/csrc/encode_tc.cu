@@ -116,6 +116,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, bool s
         else if (clock64() - t0 > 20000000000ll) __trap();  // ~10 s: a lost arrival (not a time slice)
     }
 }
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -291,24 +296,27 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
 
     if (warp == 0) {
         // ---------------- MMA issuer ----------------
-        if (lane == 0) {
-            uint32_t it = 0, jt = 0;
-            for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-                const int64_t t0 = g * gs, tn = (ntiles - t0 < gs) ? (ntiles - t0) : gs;
-                for (int j = 0; j < m; ++j, ++jt) {
-                    const int jb = jt & 1;
-                    mbar_wait(&H->b_full[jb], (jt >> 1) & 1, probe & 256);
-                    for (int t = 0; t < tn; ++t, ++it) {
-                        const int as = it % kNA, tb = it & 1;
-                        mbar_wait(&H->a_full[as], (it / kNA) & 1, probe & 256);
-                        if (stamp && it < kStampItems) stamp[it * 8 + 0] = clock64();
-                        const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
-                        for (int c = 0; c < kNC; ++c) {
-                            // chunk c of buffer tb drained by the scan of item it - 2
-                            if (it >= 2) mbar_wait(&H->t_empty[(it - 2) & 3][c], ((it - 2) >> 2) & 1, probe & 256);
-                            if (stamp && c == 0 && it < kStampItems) stamp[it * 8 + 1] = clock64();
-                            tc_fence_after();
-                            const uint32_t bc = b0 + (uint32_t)(c * (kCW / 8) * S::kRowGroupBytes);  // centroids c kCW ..
+        // The whole warp walks the items (warp-uniform descriptors live in uniform registers) and
+        // one elected lane issues: no per-thread -> uniform register waterfall around each MMA
+        // (scripts/micro/umma_rate.cu: 676 vs 756 cycles from issue to completion of an item).
+        uint32_t it = 0, jt = 0;
+        for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+            const int64_t t0 = g * gs, tn = (ntiles - t0 < gs) ? (ntiles - t0) : gs;
+            for (int j = 0; j < m; ++j, ++jt) {
+                const int jb = jt & 1;
+                mbar_wait(&H->b_full[jb], (jt >> 1) & 1, probe & 256);
+                for (int t = 0; t < tn; ++t, ++it) {
+                    const int as = it % kNA, tb = it & 1;
+                    mbar_wait(&H->a_full[as], (it / kNA) & 1, probe & 256);
+                    if (stamp && lane == 0 && it < kStampItems) stamp[it * 8 + 0] = clock64();
+                    const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
+                    for (int c = 0; c < kNC; ++c) {
+                        // chunk c of buffer tb drained by the scan of item it - 2
+                        if (it >= 2) mbar_wait(&H->t_empty[(it - 2) & 3][c], ((it - 2) >> 2) & 1, probe & 256);
+                        if (stamp && lane == 0 && c == 0 && it < kStampItems) stamp[it * 8 + 1] = clock64();
+                        tc_fence_after();
+                        const uint32_t bc = b0 + (uint32_t)(c * (kCW / 8) * S::kRowGroupBytes);  // centroids c kCW ..
+                        if (elect_one()) {
 #pragma unroll
                             for (int s = 0; s < S::kSteps; ++s) {
                                 const uint64_t da = make_desc(a0 + 2 * s * 128, 128, S::kRowGroupBytes);
@@ -317,10 +325,12 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                             }
                             mma_commit(&H->t_full[it & 3][c]);  // the last one also frees A stage `as`
                         }
-                        if (stamp && it < kStampItems) stamp[it * 8 + 2] = clock64();
+                        __syncwarp();
                     }
-                    mma_commit(&H->b_empty[jb]);
+                    if (stamp && lane == 0 && it < kStampItems) stamp[it * 8 + 2] = clock64();
                 }
+                if (elect_one()) mma_commit(&H->b_empty[jb]);
+                __syncwarp();
             }
         }
     } else if (warp == 1) {

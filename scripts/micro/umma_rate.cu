@@ -164,6 +164,81 @@ void run_lat(const char *name, long long *d) {
            a / 148 / items, b / 148 / items);
 }
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+// same as k_umma_lat, but the whole warp runs the loop and one elected lane issues
+// (warp-uniform descriptors: no per-thread -> uniform register waterfall around each MMA)
+template <int N, int KSTEPS>
+__global__ void __launch_bounds__(128, 1) k_umma_lat_warp(int items, long long *cycles) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int K = KSTEPS * 8;
+    unsigned char *sA = sm, *sB = sm + 128 * K * 4;
+    for (int i = threadIdx.x; i < (128 + N) * K; i += blockDim.x) reinterpret_cast<float *>(sm)[i] = 0.f;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tbase;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const int rg = KSTEPS * 2 * 128;
+    if (threadIdx.x < 32) {
+        long long iss = 0, lat = 0;
+        for (int it = 0; it < items; ++it) {
+            const long long t0 = clock64();
+            if (elect_one()) {
+#pragma unroll
+                for (int s = 0; s < KSTEPS; ++s) {
+                    const uint64_t da = make_desc(smem_u32(sA) + 2 * s * 128, 128, rg);
+                    const uint64_t db = make_desc(smem_u32(sB) + 2 * s * 128, 128, rg);
+                    mma<0>(tmem + (it & 1) * 256, da, db, idesc, s > 0);
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+            }
+            __syncwarp();
+            const long long t1 = clock64();
+            uint32_t done = 0;
+            while (!done)
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                             : "=r"(done) : "r"(smem_u32(&bar)), "r"((uint32_t)(it & 1)) : "memory");
+            const long long t2 = clock64();
+            iss += t1 - t0; lat += t2 - t0;
+        }
+        if (threadIdx.x == 0) { cycles[2 * blockIdx.x] = iss; cycles[2 * blockIdx.x + 1] = lat; }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+template <int N, int KSTEPS>
+void run_lat_warp(const char *name, long long *d) {
+    const int items = 512;
+    const size_t smem = (size_t)(128 + N) * KSTEPS * 8 * 4;
+    auto k = k_umma_lat_warp<N, KSTEPS>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<148, 128, smem>>>(items, d);
+    cudaError_t err = cudaDeviceSynchronize();
+    long long h[296]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    double a = 0, b = 0; for (int i = 0; i < 148; ++i) { a += h[2 * i]; b += h[2 * i + 1]; }
+    printf("%-22s %s  issue %7.1f cycles  issue->done %7.1f cycles (idle pipe, per item, warp+elect)\n", name, cudaGetErrorString(err),
+           a / 148 / items, b / 148 / items);
+}
+
 int main() {
     long long *d; cudaMalloc(&d, 296 * sizeof(long long));
     run<0, 256, 4>("tf32 N256 K32", d);
@@ -175,5 +250,7 @@ int main() {
     run_lat<256, 4>("lat tf32 N256 K32", d);
     run_lat<256, 1>("lat tf32 N256 K8", d);
     run_lat<128, 4>("lat tf32 N128 K32", d);
+    run_lat_warp<256, 4>("latw tf32 N256 K32", d);
+    run_lat_warp<256, 1>("latw tf32 N256 K8", d);
     return 0;
 }
