@@ -77,7 +77,10 @@ from ._native import NativeUnavailable
 
 __version__ = "0.1.0"
 
+from .harness import BENCH_CSV_COLUMNS, BenchResult, run_bench_matrix, run_verify, write_bench_csv  # noqa: E402
+
 __all__ = [
+    "BENCH_CSV_COLUMNS", "BenchResult", "run_bench_matrix", "run_verify", "write_bench_csv",
     "EvalReport", "adc_search", "adc_search_batched", "evaluate", "exact_topn", "mse_of", "reconstruct",
     "crc32_device", "encode_file", "read_bvecs", "read_codebooks", "read_codes", "read_fvecs", "read_ivecs",
     "synth_dataset", "write_bvecs", "write_codebooks", "write_codes", "write_fvecs", "write_ivecs",

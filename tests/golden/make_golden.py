@@ -320,14 +320,49 @@ def eval_cases():
     return out
 
 
+def verify_cases():
+    """Reference cli.run_verify (three-way encoder equivalence with the float64
+    near-tie classifier) on bisector-heavy data where REFERENCE and
+    REFORMULATED disagree."""
+    from cspq import bulk, core
+    from cspq.cli import run_verify
+    out = {}
+    rng = np.random.default_rng(3)
+    n, m, k, sub = 4000, 4, 256, 8
+    rm = np.round(rng.uniform(0, 255, (m, k, sub))).astype(np.float32)
+    X = np.empty((n, m * sub), np.float32)
+    for j in range(m):
+        a = rng.integers(0, k, n)
+        b = rng.integers(0, k, n)
+        mid = 0.5 * (rm[j, a] + rm[j, b])  # half-integers: exact float32 bisectors (ties)
+        mid[1::2] += rng.normal(0, 1e-4, (n // 2, sub))
+        X[:, j * sub:(j + 1) * sub] = mid
+    cbs = [core.Codebook.from_rowmajor(j, rm[j]) for j in range(m)]
+    # (a VectorDataset: the reference's hasattr(dataset, "data") probe breaks on raw arrays)
+    checked, near, fail, details = run_verify(core.VectorDataset(data=X), cbs, 3000, 1e-5, seed=7)
+    import zlib
+    out["v/X_crc32"], out["v/rowmajor"] = np.int64(zlib.crc32(X.tobytes())), rm  # X is regenerated by the test
+    out["v/counts"] = np.array([checked, near, fail], np.int64)
+    out["v/ij"] = np.array([(i, j) for i, j, *_ in details], np.int64).reshape(-1, 2)
+    out["v/near"] = np.array([kind == "near-tie" for _, _, kind, _, _ in details], bool)
+    out["v/gap"] = np.array([gap for _, _, _, gap, _ in details], np.float64)
+    out["v/codes"] = np.array([[c["REFERENCE"], c["REFORMULATED"], c["BLOCKED"]] for *_, c in details],
+                              np.int64).reshape(-1, 3)
+    return out
+
+
 def main():
     bulk, core, kernels, training = _ref()
+    if sys.argv[1:] == ["verify"]:  # (added later: regenerate only this archive)
+        np.savez_compressed(os.path.join(HERE, "verify_golden.npz"), **verify_cases())
+        return
     np.savez_compressed(os.path.join(HERE, "encode_golden.npz"), **encode_cases(bulk, core, kernels))
     np.savez_compressed(os.path.join(HERE, "lloyd_golden.npz"), **lloyd_cases(training))
     np.savez_compressed(os.path.join(HERE, "train_golden.npz"), **train_cases(core, training))
     np.savez_compressed(os.path.join(HERE, "pairwise_golden.npz"), **pairwise_cases())
     np.savez_compressed(os.path.join(HERE, "io_golden.npz"), **io_cases())
     np.savez_compressed(os.path.join(HERE, "eval_golden.npz"), **eval_cases())
+    np.savez_compressed(os.path.join(HERE, "verify_golden.npz"), **verify_cases())
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
