@@ -243,9 +243,10 @@ struct TcSmem {
 // ------------------------------------------------------------------ the kernel
 template <int SUB, typename TIn>
 __global__ void __launch_bounds__(kThreads, 1)
-encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const float *__restrict__ CB,
+encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_t xjs, const float *__restrict__ CB,
                  const float *__restrict__ Bv, const float *__restrict__ guard, const uint8_t *__restrict__ img,
-                 uint8_t *__restrict__ codes, int64_t cs, float *__restrict__ best_out, int gs, int probe) {
+                 uint8_t *__restrict__ codes, int64_t cs, int64_t cjs, uint8_t *__restrict__ flags,
+                 float *__restrict__ best_out, int gs, int probe) {
     // (a build with the probe / stamp tests folded away measured 7 % slower on c3: its schedule
     // spills at the 128-register cap, so the runtime-uniform tests stay)
     // probe (debug timing only): bit 0 = epilogue skips its min work, bit 1 = no MMAs,
@@ -366,7 +367,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
         auto prefetch = [&](const ItemIter &pi, uint32_t item) {
             const int64_t row = pi.tile() * kTM + r;
             const bool ok = pi.valid() && row < n;
-            const TIn *src = X + (ok ? row * xs + (int64_t)pi.j * SUB : 0);
+            const TIn *src = X + (ok ? row * xs + (int64_t)pi.j * xjs : 0);
             unsigned char *dst = ring(item);
             constexpr int bytes = SUB * (int)sizeof(TIn);
             if constexpr (bytes == 32) {
@@ -511,7 +512,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             norm_cur = norm_next;
             if (probe & 128) {  // (timing probe: no selection / fix-up; garbage codes)
                 const int64_t row = ii.tile() * kTM + r;
-                if (row < n && !(probe & 64)) codes[row * cs + j] = (uint8_t)(__float_as_uint(cls[0] + xnorm) & 255);
+                if (row < n && !(probe & 64)) codes[row * cs + j * cjs] = (uint8_t)(__float_as_uint(cls[0] + xnorm) & 255);
                 continue;
             }
             float bm[32];
@@ -552,7 +553,12 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
             const bool flag = (row < n) && !(ncf == 1.0f && nbf == 1.0f);
             // exact warp-cooperative re-encode of flagged rows (x and the fp32 codebook from
             // shared memory: the item's x slot stays valid until kPD more owned items)
-            unsigned mask = __ballot_sync(0xffffffffu, flag && !(probe & 15));
+            if (flags) {  // mark mode (Lloyd screening): flagged rows are settled by the caller
+                if (row < n) flags[row * cs + j * cjs] = flag ? 1 : 0;
+                const unsigned fm = __ballot_sync(0xffffffffu, flag);
+                if (lane == 0 && fm) atomicAdd(&g_tc_flagged, (unsigned long long)__popc(fm));
+            }
+            unsigned mask = __ballot_sync(0xffffffffu, flag && !(probe & 15) && !flags);
             if (mask) {
                 // acquire the bulk copies of this pair (the buffer cannot advance past this
                 // pair until every epilogue thread has arrived on b_empty)
@@ -587,7 +593,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, const 
                 }
             }
             if (row < n) {
-                if (!(probe & 64)) codes[row * cs + j] = (uint8_t)code;
+                if (!(probe & 64)) codes[row * cs + j * cjs] = (uint8_t)code;
                 if (best_out) best_out[row * m + j] = m1;
             }
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 7] = clock64();
@@ -637,8 +643,8 @@ __global__ void tc_image_kernel(const float *__restrict__ CB, const float *__res
 }
 
 template <int SUB, typename TIn>
-int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, const float *CB, const float *B, const float *guard,
-              const uint8_t *img, uint8_t *codes, int64_t cs, float *best, cudaStream_t st) {
+int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const float *CB, const float *B, const float *guard,
+              const uint8_t *img, uint8_t *codes, int64_t cs, int64_t cjs, uint8_t *flags, float *best, cudaStream_t st) {
     const size_t smem = TcSmem<SUB, TIn>::total(m);
     CSPQ_REQUIRE(smem <= 227 * 1024, CSPQ_E_CONFIG, "too many subspaces (%d) for the tensor-core kernel", m);
     const char *pe = getenv("CSPQ_TC_PROBE");  // debug timing knob (instrumented variant), see the kernel
@@ -662,7 +668,7 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, const float *CB, const
     if (const char *ge = getenv("CSPQ_TC_GS")) gs = std::max(1, std::min(kG, atoi(ge)));  // debug override
     const int64_t ngroups = (ntiles + gs - 1) / gs;
     const int grid = (int)std::min<int64_t>(sms, ngroups);
-    kern<<<grid, kThreads, smem, st>>>(X, n, m, xs, CB, B, guard, img, codes, cs, best, gs, probe);
+    kern<<<grid, kThreads, smem, st>>>(X, n, m, xs, xjs, CB, B, guard, img, codes, cs, cjs, flags, best, gs, probe);
     CSPQ_LAUNCH_CHECK();
     return CSPQ_OK;
 }
@@ -683,22 +689,32 @@ int encode_tc_prepare(const float *CB, const float *B, int m, int k, int sub, vo
     return CSPQ_OK;
 }
 
-int encode_tc(const void *X, int in_dtype, int64_t n, int64_t xrs, const float *CB, const float *B,
-              const float *guard, const void *img, int m, int k, int sub, uint8_t *codes, int64_t crs, float *best,
-              cudaStream_t st) {
+// xjs / cjs: element strides between subspaces of a row in X and in codes (sub and 1 for
+// row-major (n, d) rows and (n, m) codes; n * sub and n for subspace-major Lloyd points and
+// assignments).  flags != nullptr: mark mode -- flagged (row, subspace) pairs get flag 1 and
+// an unspecified code instead of the exact fix-up (the caller settles them).
+int encode_tc_ex(const void *X, int in_dtype, int64_t n, int64_t xrs, int64_t xjs, const float *CB, const float *B,
+                 const float *guard, const void *img, int m, int k, int sub, uint8_t *codes, int64_t crs, int64_t cjs,
+                 uint8_t *flags, float *best, cudaStream_t st) {
     CSPQ_REQUIRE(k == kN && (sub == 4 || sub == 8), CSPQ_E_CONFIG,
                  "tensor-core encode needs k=256 and sub in {4, 8} (got k=%d, sub=%d)", k, sub);
     const uint8_t *im = reinterpret_cast<const uint8_t *>(img);
     if (in_dtype == CSPQ_IN_U8) {
         const uint8_t *x = reinterpret_cast<const uint8_t *>(X);
-        return sub == 8 ? launch_tc<8, uint8_t>(x, n, m, xrs, CB, B, guard, im, codes, crs, best, st)
-                        : launch_tc<4, uint8_t>(x, n, m, xrs, CB, B, guard, im, codes, crs, best, st);
+        return sub == 8 ? launch_tc<8, uint8_t>(x, n, m, xrs, xjs, CB, B, guard, im, codes, crs, cjs, flags, best, st)
+                        : launch_tc<4, uint8_t>(x, n, m, xrs, xjs, CB, B, guard, im, codes, crs, cjs, flags, best, st);
     }
     const float *x = reinterpret_cast<const float *>(X);
-    CSPQ_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0 && (xrs * 4) % 16 == 0, CSPQ_E_CONFIG,
+    CSPQ_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0 && (xrs * 4) % 16 == 0 && (xjs * 4) % 16 == 0, CSPQ_E_CONFIG,
                  "tensor-core encode needs 16-byte aligned float32 rows");
-    return sub == 8 ? launch_tc<8, float>(x, n, m, xrs, CB, B, guard, im, codes, crs, best, st)
-                    : launch_tc<4, float>(x, n, m, xrs, CB, B, guard, im, codes, crs, best, st);
+    return sub == 8 ? launch_tc<8, float>(x, n, m, xrs, xjs, CB, B, guard, im, codes, crs, cjs, flags, best, st)
+                    : launch_tc<4, float>(x, n, m, xrs, xjs, CB, B, guard, im, codes, crs, cjs, flags, best, st);
+}
+
+int encode_tc(const void *X, int in_dtype, int64_t n, int64_t xrs, const float *CB, const float *B,
+              const float *guard, const void *img, int m, int k, int sub, uint8_t *codes, int64_t crs, float *best,
+              cudaStream_t st) {
+    return encode_tc_ex(X, in_dtype, n, xrs, sub, CB, B, guard, img, m, k, sub, codes, crs, 1, nullptr, best, st);
 }
 
 int encode_tc_stats(unsigned long long *flagged, int reset) {

@@ -41,6 +41,8 @@ struct WsLayout {
     int64_t counts, sums, obj, prev, state, empties, nempty, assign_it;
     // float32 copy of float64 points (final pass), k-means++ scratch
     int64_t p32, d2, pp;
+    // tensor-core screened assignment: float32 codebooks, biases, guard, tcgen05 image, codes, flags
+    int64_t tc_cb, tc_b, tc_guard, tc_img, tc_codes, tc_flags;
     int64_t total;
     int64_t nch, maxleaves;
     WsLayout(int64_t n, int m, int sub, int k) {
@@ -72,6 +74,12 @@ struct WsLayout {
         p32 = take(4 * (int64_t)m * n * sub);
         d2 = take(8 * (int64_t)m * n);
         pp = take(8 * (int64_t)m * n);
+        tc_cb = take(4 * (int64_t)m * k * sub);
+        tc_b = take(4 * (int64_t)m * k);
+        tc_guard = take(8 * (int64_t)m);
+        tc_img = take((int64_t)m * k * 32 * 4);  // K = 32 tf32 per centroid row at most
+        tc_codes = take((int64_t)m * n);
+        tc_flags = take((int64_t)m * n);
         total = o;
     }
     template <typename T>
@@ -366,6 +374,69 @@ assign_kernel(const TP *__restrict__ P, int64_t n, int k, int sub_rt, const doub
 }
 
 // ---------------------------------------------------------------- counting sort
+// ---------------------------------------------------------------- tensor-core screened assignment
+// The float64 argmin of d_l = ||c_l||^2 - 2 x.c_l is the argmin of the real score
+// b_l - x.c_l (b = ||c||^2 / 2).  The tcgen05 encode kernel evaluates that score from
+// float32(c), float32(b) with the error band E of the encode path and flags every point whose
+// runner-up lies within 4E; rounding c and b to float32 moves a score by at most 2^-24 W
+// (W = |b| + ||x|| ||c||, far inside the 2x margin of the 4E threshold), so an unflagged
+// point's winner is the real -- and float64 -- argmin by a margin no float64 rounding can
+// close.  Flagged points (~1e-3) take the full float64 scan; every point's d and sq come from
+// the same float64 chain as assign_kernel, so assignments and objective terms are identical.
+__global__ void tc_codebook_kernel(const double *__restrict__ C64, const double *__restrict__ cn, int k, int sub,
+                                   float *__restrict__ cb32, float *__restrict__ b32) {
+    const int j = blockIdx.x;
+    for (int l = threadIdx.x; l < k; l += blockDim.x) {
+        const int64_t i = (int64_t)j * k + l;
+        for (int t = 0; t < sub; ++t) cb32[i * sub + t] = __double2float_rn(C64[i * sub + t]);
+        b32[i] = __double2float_rn(0.5 * cn[i]);
+    }
+}
+
+template <int SUBC>
+__global__ void __launch_bounds__(256)
+tc_settle_kernel(const float *__restrict__ P, int64_t n, int k, const double *__restrict__ C64,
+                 const double *__restrict__ cn_g, const int32_t *__restrict__ state, int64_t b, int64_t e,
+                 const uint8_t *__restrict__ codes, const uint8_t *__restrict__ flags, int32_t *__restrict__ assign,
+                 double *__restrict__ sq) {
+    const int j = blockIdx.y;
+    if (!state[j]) return;
+    const double *Cj = C64 + (int64_t)j * k * SUBC;
+    const double *cnj = cn_g + (int64_t)j * k;
+    for (int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ji = (int64_t)j * n + i;
+        double x[SUBC];
+#pragma unroll
+        for (int t = 0; t < SUBC; ++t) x[t] = (double)P[ji * SUBC + t];
+        int bi;
+        double best;
+        auto dist = [&](int l) {
+            const double *c = Cj + (int64_t)l * SUBC;
+            double dot = 0.0;
+#pragma unroll
+            for (int t = 0; t < SUBC; ++t) dot = __fma_rn(x[t], c[t], dot);
+            return __fma_rn(-2.0, dot, cnj[l]);
+        };
+        if (flags[ji]) {  // full float64 scan, first index on ties (assign_kernel's order)
+            best = 0.0;
+            bi = 0;
+            for (int l = 0; l < k; ++l) {
+                const double d1 = dist(l);
+                if (l == 0 || d1 < best) { best = d1; bi = l; }
+            }
+        } else {
+            bi = codes[ji];
+            best = dist(bi);
+        }
+        double xx = 0.0;
+#pragma unroll
+        for (int t = 0; t < SUBC; ++t) xx = __dadd_rn(xx, __dmul_rn(x[t], x[t]));
+        const double v = __dadd_rn(best, xx);
+        assign[ji] = bi;
+        sq[ji] = (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(v, 0.0)
+    }
+}
+
 __global__ void hist_kernel(const int32_t *__restrict__ assign, int64_t n, int k, const int32_t *state,
                             int64_t b, int64_t e, int64_t nch, int32_t *__restrict__ hist, int use_smem) {
     const int j = blockIdx.y;
@@ -772,6 +843,37 @@ size_t lloyd_workspace_bytes(int64_t n, int m, int sub, int k) { return (size_t)
         else { using TP = float; const TP *Pt = reinterpret_cast<const TP *>(P); __VA_ARGS__; }       \
     } while (0)
 
+int encode_prepare(const float *CB, const float *B, int m, int k, int sub, float *guard, cudaStream_t st);
+int encode_tc_prepare(const float *CB, const float *B, int m, int k, int sub, void *img, cudaStream_t st);
+int encode_tc_ex(const void *X, int in_dtype, int64_t n, int64_t xrs, int64_t xjs, const float *CB, const float *B,
+                 const float *guard, const void *img, int m, int k, int sub, uint8_t *codes, int64_t crs, int64_t cjs,
+                 uint8_t *flags, float *best, cudaStream_t st);
+
+// assignment of points [b, e) of every subspace through the tcgen05 encode kernel in mark
+// mode, then tc_settle_kernel (see above)
+static int assign_tc(const float *P, int64_t n, int m, int sub, int k, const double *C64, const double *cn,
+                     const int32_t *state, int64_t b, int64_t e, int32_t *assign, double *sq, void *ws,
+                     const WsLayout &L, cudaStream_t st) {
+    float *cb32 = L.at<float>(ws, L.tc_cb), *b32 = L.at<float>(ws, L.tc_b), *guard = L.at<float>(ws, L.tc_guard);
+    void *img = L.at<void>(ws, L.tc_img);
+    uint8_t *codes = L.at<uint8_t>(ws, L.tc_codes), *flags = L.at<uint8_t>(ws, L.tc_flags);
+    tc_codebook_kernel<<<m, 256, 0, st>>>(C64, cn, k, sub, cb32, b32);
+    CSPQ_LAUNCH_CHECK();
+    int rc;
+    if ((rc = encode_prepare(cb32, b32, m, k, sub, guard, st))) return rc;
+    if ((rc = encode_tc_prepare(cb32, b32, m, k, sub, img, st))) return rc;
+    // rows = points b.. of every subspace: row stride sub, subspace stride n * sub; codes and
+    // flags subspace-major (m, n) like assign
+    if ((rc = encode_tc_ex(P + b * sub, CSPQ_IN_F32, e - b, sub, n * sub, cb32, b32, guard, img, m, k, sub, codes + b, 1, n,
+                           flags + b, nullptr, st)))
+        return rc;
+    dim3 grid((unsigned)grid_for(e - b, 256, 148 * 8), (unsigned)m);
+    if (sub == 8) tc_settle_kernel<8><<<grid, 256, 0, st>>>(P, n, k, C64, cn, state, b, e, codes, flags, assign, sq);
+    else tc_settle_kernel<4><<<grid, 256, 0, st>>>(P, n, k, C64, cn, state, b, e, codes, flags, assign, sq);
+    CSPQ_LAUNCH_CHECK();
+    return CSPQ_OK;
+}
+
 int lloyd_assign(const void *P, int pf64, int64_t n, int m, int sub, int k, const double *C64,
                  const int32_t *state, int64_t b, int64_t e, int32_t *assign, double *sq, void *ws, cudaStream_t st) {
     WsLayout L(n, m, sub, k);
@@ -780,6 +882,10 @@ int lloyd_assign(const void *P, int pf64, int64_t n, int m, int sub, int k, cons
     cnorm_kernel<<<(unsigned)((mk + 255) / 256), 256, 0, st>>>(C64, m, k, sub, state, cn);
     CSPQ_LAUNCH_CHECK();
     if (e <= b) return CSPQ_OK;
+    const char *tcv = getenv("CSPQ_LLOYD_TC");  // "0": the plain float64 kernel (A/B and tests)
+    const bool tc_on = !(tcv && tcv[0] == '0');
+    if (tc_on && !pf64 && k == 256 && (sub == 4 || sub == 8) && reinterpret_cast<uintptr_t>(P) % 16 == 0)
+        return assign_tc(reinterpret_cast<const float *>(P), n, m, sub, k, C64, cn, state, b, e, assign, sq, ws, L, st);
     const size_t need = (size_t)k * (sub + 1) * sizeof(double);
     const int use_smem = need <= 96 * 1024;
     const size_t smem = use_smem ? need : 0;

@@ -209,3 +209,43 @@ def test_sharded_driver_matches_batched_lloyd(P):
             assert a.centroids.tobytes() == b.centroids.tobytes()
             assert a.objectives == b.objectives
             assert np.array_equal(a.assignments, b.assignments)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_tensor_screened_assignment_equals_float64(P, monkeypatch, name):
+    """k = 256, sub in {4, 8}: the assignment runs through the tcgen05 encode
+    kernel (mark mode) plus a float64 settle of flagged points.  Every
+    subspace's centroids, objectives, iterations and final assignments equal
+    the plain float64 kernel's (CSPQ_LLOYD_TC=0) bit for bit."""
+    import torch
+    from paper_2605_25521_b200 import configs as C
+    cfg = C.CONFIGS[name].scaled(n=200_000, n_train=50_000)
+    S = C.training_sample(cfg, torch.device("cuda", 0))
+    Ssm = C.subspace_major(S, cfg.m)
+    init = C.lloyd_init(cfg, Ssm)
+    tc = P.TrainConfig(k=cfg.k, max_iters=cfg.iters, tol=0.0)
+    monkeypatch.setenv("CSPQ_LLOYD_TC", "0")
+    ref = P.lloyd_iterate_batched(Ssm, init, tc)
+    monkeypatch.setenv("CSPQ_LLOYD_TC", "1")
+    got = P.lloyd_iterate_batched(Ssm, init, tc)
+    for j in range(cfg.m):
+        assert got[j].centroids.tobytes() == ref[j].centroids.tobytes(), (name, j)
+        assert got[j].objectives == ref[j].objectives and got[j].iterations == ref[j].iterations
+        assert np.array_equal(got[j].assignments, ref[j].assignments)
+
+
+def test_tensor_screened_assignment_ties(P, monkeypatch, oracle):
+    """Heavy exact ties (few distinct points, duplicated initial centroids,
+    empty clusters): flagged points settle in float64 with the first index."""
+    rng = np.random.default_rng(5)
+    m, n, sub, k = 2, 6000, 8, 256
+    base = np.round(rng.uniform(-3, 3, (40, sub))).astype(np.float32)
+    pts = np.ascontiguousarray(base[rng.integers(0, 40, (m, n))])
+    init = np.ascontiguousarray(pts[:, rng.integers(0, n, k)].astype(np.float64))
+    tc = P.TrainConfig(k=k, max_iters=6, tol=0.0)
+    monkeypatch.setenv("CSPQ_LLOYD_TC", "1")
+    got = P.lloyd_iterate_batched(pts, init, tc)
+    for j in range(m):
+        o = oracle.lloyd(pts[j].astype(np.float64), init[j], 6, 0.0)
+        assert got[j].centroids.tobytes() == o["centroids"].tobytes()
+        assert got[j].objectives == o["objectives"]
