@@ -393,7 +393,7 @@ __global__ void tc_codebook_kernel(const double *__restrict__ C64, const double 
     }
 }
 
-template <int SUBC>
+template <int SUBC>  // k == 256
 __global__ void __launch_bounds__(256)
 tc_settle_kernel(const float *__restrict__ P, int64_t n, int k, const double *__restrict__ C64,
                  const double *__restrict__ cn_g, const int32_t *__restrict__ state, int64_t b, int64_t e,
@@ -401,8 +401,14 @@ tc_settle_kernel(const float *__restrict__ P, int64_t n, int k, const double *__
                  double *__restrict__ sq) {
     const int j = blockIdx.y;
     if (!state[j]) return;
-    const double *Cj = C64 + (int64_t)j * k * SUBC;
-    const double *cnj = cn_g + (int64_t)j * k;
+    // the subspace's float64 codebook and norms in shared memory (k = 256: 8-16 KB + 2 KB);
+    // every point gathers one centroid from it
+    __shared__ double sC[256 * SUBC], scn[256];
+    for (int q = threadIdx.x; q < k * SUBC; q += blockDim.x) sC[q] = C64[(int64_t)j * k * SUBC + q];
+    for (int q = threadIdx.x; q < k; q += blockDim.x) scn[q] = cn_g[(int64_t)j * k + q];
+    __syncthreads();
+    const double *Cj = sC;
+    const double *cnj = scn;
     for (int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t ji = (int64_t)j * n + i;
         double x[SUBC];
@@ -867,7 +873,8 @@ static int assign_tc(const float *P, int64_t n, int m, int sub, int k, const dou
     if ((rc = encode_tc_ex(P + b * sub, CSPQ_IN_F32, e - b, sub, n * sub, cb32, b32, guard, img, m, k, sub, codes + b, 1, n,
                            flags + b, nullptr, st)))
         return rc;
-    dim3 grid((unsigned)grid_for(e - b, 256, 148 * 8), (unsigned)m);
+    // ~8 CTAs per SM in total: each CTA stages its subspace's codebook once for many points
+    dim3 grid((unsigned)grid_for(e - b, 256, std::max<int64_t>(1, 148 * 8 / m)), (unsigned)m);
     if (sub == 8) tc_settle_kernel<8><<<grid, 256, 0, st>>>(P, n, k, C64, cn, state, b, e, codes, flags, assign, sq);
     else tc_settle_kernel<4><<<grid, 256, 0, st>>>(P, n, k, C64, cn, state, b, e, codes, flags, assign, sq);
     CSPQ_LAUNCH_CHECK();
