@@ -249,3 +249,31 @@ def test_tensor_screened_assignment_ties(P, monkeypatch, oracle):
         o = oracle.lloyd(pts[j].astype(np.float64), init[j], 6, 0.0)
         assert got[j].centroids.tobytes() == o["centroids"].tobytes()
         assert got[j].objectives == o["objectives"]
+
+
+def test_screened_assignment_on_row_ranges(P, monkeypatch):
+    """cspq_lloyd_assign over disjoint point ranges [b, e) (the row-sharded
+    driver's call) equals one full-range call and the plain float64 kernel."""
+    import torch
+    from paper_2605_25521_b200.distributed import CudaSteps
+    rng = np.random.default_rng(21)
+    m, n, sub, k = 3, 10_001, 8, 256
+    dev = torch.device("cuda", 0)
+    pts = torch.from_numpy(rng.standard_normal((m, n, sub)).astype(np.float32)).to(dev)
+    C64 = torch.from_numpy(rng.standard_normal((m, k, sub))).to(dev)
+    state = torch.ones(m, dtype=torch.int32, device=dev)
+    steps = CudaSteps(pts, 0, n, m, sub, k, dev)
+
+    def run(ranges, tc):
+        monkeypatch.setenv("CSPQ_LLOYD_TC", tc)
+        a = torch.full((m, n), -1, dtype=torch.int32, device=dev)
+        s = torch.full((m, n), -1.0, dtype=torch.float64, device=dev)
+        for b, e in ranges:
+            steps.assign(C64, state, b, e, a, s)
+        torch.cuda.synchronize()
+        return a.cpu().numpy(), s.cpu().numpy()
+
+    full = run([(0, n)], "0")
+    for ranges in ([(0, n)], [(0, 3000), (3000, 7777), (7777, n)], [(5, 133), (0, 5), (133, n)]):
+        got = run(ranges, "1")
+        assert np.array_equal(got[0], full[0]) and got[1].tobytes() == full[1].tobytes(), ranges
