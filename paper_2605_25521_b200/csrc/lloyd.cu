@@ -24,6 +24,11 @@
 //     subspace (state[j]) so every subspace runs exactly the iterations the
 //     reference's sequential loop would.
 
+#include <map>
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 
 namespace cspq {
@@ -99,10 +104,9 @@ struct WsHeader {
 // Also the internal nodes of that recursion (node = left + right, exactly numpy's order),
 // grouped by height so that a CTA can evaluate them level by level.  Node ids: leaves are
 // 0 .. nl-1 (in order), internal nodes nl .. in construction order.  Built once per n.
-__global__ void leaves_kernel(int64_t n, int64_t *leaves, int32_t *nodes, int32_t *ntmp, int64_t maxleaves,
-                              WsHeader *hdr) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (hdr->magic == kMagic && hdr->leaves_for == n) return;
+// (host code: the tree depends on n only, so it is built once per (device, n) on the host and
+// kept in device memory -- a single GPU thread took 6 ms for n = 1M)
+void build_tree(int64_t n, int64_t *leaves, int32_t *nodes, int32_t *ntmp, int64_t maxleaves, WsHeader *hdr) {
     // pass 1: leaves in order
     struct F { int64_t lo, len; };
     F st[96];
@@ -183,6 +187,37 @@ __global__ void leaves_kernel(int64_t n, int64_t *leaves, int32_t *nodes, int32_
     hdr->nlevels = maxh;  // off[h] = end of level h; level 1 starts at 0
 }
 
+struct TreeBuf {
+    int64_t *leaves;
+    int32_t *nodes;
+    const WsHeader *hdr;
+};
+// leaves (16 B x maxleaves) | nodes (8 B x maxleaves + 320 B) | header, in device memory
+TreeBuf tree_for(int64_t n) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int64_t>, TreeBuf> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({dev, n});
+    if (it != cache.end()) return it->second;
+    const int64_t maxleaves = n / 32 + 8;
+    const size_t lb = 16 * (size_t)maxleaves, nb = 8 * (size_t)maxleaves + 4 * 80;
+    std::vector<unsigned char> h(lb + nb + sizeof(WsHeader));
+    std::vector<int32_t> ntmp(3 * (size_t)maxleaves);
+    build_tree(n, reinterpret_cast<int64_t *>(h.data()), reinterpret_cast<int32_t *>(h.data() + lb), ntmp.data(),
+               maxleaves, reinterpret_cast<WsHeader *>(h.data() + lb + nb));
+    unsigned char *d = nullptr;
+    if (cudaMalloc(&d, h.size()) != cudaSuccess || cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        if (d) cudaFree(d);
+        return {nullptr, nullptr, nullptr};
+    }
+    TreeBuf t{reinterpret_cast<int64_t *>(d), reinterpret_cast<int32_t *>(d + lb),
+              reinterpret_cast<const WsHeader *>(d + lb + nb)};
+    cache[{dev, n}] = t;
+    return t;
+}
+
 // numpy leaf sum: <8 sequential from 0.0; else 8 accumulators, fixed combine, tail
 __device__ double leaf_sum(const double *a, int64_t n) {
     if (n < 8) {
@@ -218,7 +253,8 @@ __global__ void leafsum_kernel(const double *vals, int64_t vstride, int64_t begi
 // evaluate the internal nodes level by level (one CTA per subspace); node ids are
 // translated to storage: id < nl -> leafsum, else nodeval[id - nl] at its sorted slot
 __global__ void combine_levels_kernel(int m, const int32_t *state, const double *leafsum, int64_t maxleaves,
-                                      const int32_t *nodes, const WsHeader *hdr, double *nodeval, double *out) {
+                                      const int32_t *nodes, int64_t tree_maxleaves, const WsHeader *hdr, double *nodeval,
+                                      double *out) {
     const int j = blockIdx.x;
     if (state && !state[j]) return;
     const int64_t nl = hdr->nleaves;
@@ -229,7 +265,7 @@ __global__ void combine_levels_kernel(int m, const int32_t *state, const double 
         if (threadIdx.x == 0) out[j] = ls[0];
         return;
     }
-    const int32_t *off = nodes + 2 * maxleaves;  // level ends
+    const int32_t *off = nodes + 2 * tree_maxleaves;  // level ends (after the tree's node pairs)
     int32_t lo = 0;
     for (int h = 1; h <= H; ++h) {
         const int32_t hi = off[h];
@@ -823,17 +859,17 @@ int grid_for(int64_t items, int threads, int64_t cap = 148 * 16) {
 // pairwise objective of vals[j][begin .. begin+len) for every active subspace
 int pairwise_obj(const double *vals, int64_t vstride, int64_t begin, int64_t len, int m,
                  const int32_t *state, void *ws, const WsLayout &L, double *out, cudaStream_t st) {
-    WsHeader *hdr = L.at<WsHeader>(ws, L.header);
-    int64_t *leaves = L.at<int64_t>(ws, L.leaves);
     double *leafsum = L.at<double>(ws, L.leafsum);
-    int32_t *nodes = L.at<int32_t>(ws, L.nodes);
-    leaves_kernel<<<1, 1, 0, st>>>(len, leaves, nodes, L.at<int32_t>(ws, L.ntmp), L.maxleaves, hdr);
-    CSPQ_LAUNCH_CHECK();
+    const TreeBuf tb = tree_for(len);
+    CSPQ_REQUIRE(tb.hdr, CSPQ_E_CUDA, "pairwise summation tree for n=%lld: device allocation failed", (long long)len);
+    const int64_t *leaves = tb.leaves;
+    const int32_t *nodes = tb.nodes;
+    const WsHeader *hdr = tb.hdr;
     const int64_t maxl = len / 32 + 8;
     dim3 g((unsigned)grid_for(maxl, 128, 64), (unsigned)m);
     leafsum_kernel<<<g, 128, 0, st>>>(vals, vstride, begin, m, state, leaves, hdr, L.maxleaves, leafsum);
     CSPQ_LAUNCH_CHECK();
-    combine_levels_kernel<<<m, 256, 0, st>>>(m, state, leafsum, L.maxleaves, nodes, hdr,
+    combine_levels_kernel<<<m, 256, 0, st>>>(m, state, leafsum, L.maxleaves, nodes, len / 32 + 8, hdr,
                                              L.at<double>(ws, L.nodeval), out);
     CSPQ_LAUNCH_CHECK();
     return CSPQ_OK;
