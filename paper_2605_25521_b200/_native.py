@@ -15,7 +15,8 @@ import subprocess
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libcspq_b200.so")
+# CSPQ_LIB_PATH: load another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("CSPQ_LIB_PATH") or os.path.join(HERE, "_lib", "libcspq_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "cspq_b200.h")
 
 CSPQ_OK = 0
