@@ -191,28 +191,20 @@ struct TcSmemHdr {
     uint32_t tmem_base;
 };
 
-// walk of the (row group, subspace, tile) work items of one CTA
+// walk of the (row group, subspace, tile) work items of one CTA (32-bit counters: the launch
+// checks ntiles < 2^31; tile() widens)
 struct ItemIter {
-    int64_t g, ngroups, ntiles;
+    int g, ngroups, ntiles;
     int j, t, m, tn, gs;  // gs: tiles per row group
     uint32_t jt;  // (row group, subspace) pairs started before the current one
-    __device__ ItemIter(int64_t g0, int64_t ng, int64_t nt, int m_, int gs_)
+    __device__ ItemIter(int g0, int ng, int nt, int m_, int gs_)
         : g(g0), ngroups(ng), ntiles(nt), j(0), t(0), m(m_), tn(0), gs(gs_), jt(0) {
-        tn = g < ng ? (int)((nt - g * gs < gs) ? (nt - g * gs) : gs) : 0;
+        tn = g < ng ? min(nt - g * gs, gs) : 0;
     }
     __device__ bool valid() const { return g < ngroups; }
-    __device__ int64_t tile() const { return g * gs + t; }
-    __device__ void next(int64_t stride) {
-        if (++t < tn) return;
-        t = 0;
-        ++jt;
-        if (++j < m) return;
-        j = 0;
-        g += stride;
-        tn = g < ngroups ? (int)((ntiles - g * gs < gs) ? (ntiles - g * gs) : gs) : 0;
-    }
-    // k items ahead (jt counts every pair boundary crossed, as k calls of next() would)
-    __device__ void advance(int k, int64_t stride) {
+    __device__ int64_t tile() const { return (int64_t)g * gs + t; }
+    // k items ahead (jt counts every pair boundary crossed, as k single steps would)
+    __device__ void advance(int k, int stride) {
         t += k;
         while (g < ngroups && t >= tn) {
             t -= tn;
@@ -220,7 +212,7 @@ struct ItemIter {
             if (++j >= m) {
                 j = 0;
                 g += stride;
-                tn = g < ngroups ? (int)((ntiles - g * gs < gs) ? (ntiles - g * gs) : gs) : 0;
+                tn = g < ngroups ? min(ntiles - g * gs, gs) : 0;
             }
         }
     }
@@ -436,7 +428,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 
         // The group walks its own items only (item e, e + kGroups, ...); ic / ip run kGroups
         // and kGroups kPD items ahead for the A conversion and the x prefetch.
-        ItemIter ii(blockIdx.x, ngroups, ntiles, m, gs);
+        ItemIter ii(blockIdx.x, (int)ngroups, (int)ntiles, m, gs);
         ii.advance(e, gridDim.x);
         ItemIter ip = ii;
         uint32_t ipi = e;
@@ -647,6 +639,7 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const flo
               const uint8_t *img, uint8_t *codes, int64_t cs, int64_t cjs, uint8_t *flags, float *best, cudaStream_t st) {
     const size_t smem = TcSmem<SUB, TIn>::total(m);
     CSPQ_REQUIRE(smem <= 227 * 1024, CSPQ_E_CONFIG, "too many subspaces (%d) for the tensor-core kernel", m);
+    CSPQ_REQUIRE((n + kTM - 1) / kTM < ((int64_t)1 << 31), CSPQ_E_CONFIG, "too many rows (%lld) for one launch", (long long)n);
     const char *pe = getenv("CSPQ_TC_PROBE");  // debug timing knob (instrumented variant), see the kernel
     const int probe = pe ? atoi(pe) : 0;
     auto kern = encode_tc_kernel<SUB, TIn>;
