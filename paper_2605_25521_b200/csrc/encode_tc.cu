@@ -247,7 +247,11 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
     // bit 5 = no x prefetch (stale x), bit 6 = no code stores
     using S = TcShape<SUB>;
     using L = TcSmem<SUB, TIn>;
+#ifdef CSPQ_TC_STAMPS
     long long *stamp = (probe & 16) && blockIdx.x == 0 ? reinterpret_cast<long long *>(best_out) : nullptr;
+#else
+    constexpr long long *stamp = nullptr;  // clock stamps: build with -DCSPQ_TC_STAMPS (scripts/stamp_tc.py)
+#endif
     if (probe & 16) best_out = nullptr;
     constexpr int kStampItems = 2048;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
