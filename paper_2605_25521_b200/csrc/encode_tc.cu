@@ -239,9 +239,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                  const float *__restrict__ Bv, const float *__restrict__ guard, const uint8_t *__restrict__ img,
                  uint8_t *__restrict__ codes, int64_t cs, int64_t cjs, uint8_t *__restrict__ flags,
                  float *__restrict__ best_out, int gs, int probe) {
-    // (a build with the probe / stamp tests folded away measured 7 % slower on c3: its schedule
-    // spills at the 128-register cap, so the runtime-uniform tests stay)
-    // probe (debug timing only): bit 0 = epilogue skips its min work, bit 1 = no MMAs,
+    // probe (debug timing only; honoured by -DCSPQ_TC_PROBES builds): bit 0 = epilogue skips its min work, bit 1 = no MMAs,
     // bit 2 = skip the A conversion, bit 3 = keep TMEM loads but skip the min work
     // (bits 0-3 leave garbage codes), bit 4 = CTA 0 writes clock64 stamps into best_out,
     // bit 5 = no x prefetch (stale x), bit 6 = no code stores
@@ -251,6 +249,12 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
     long long *stamp = (probe & 16) && blockIdx.x == 0 ? reinterpret_cast<long long *>(best_out) : nullptr;
 #else
     constexpr long long *stamp = nullptr;  // clock stamps: build with -DCSPQ_TC_STAMPS (scripts/stamp_tc.py)
+#endif
+#ifndef CSPQ_TC_PROBES
+    // timing probes: build with -DCSPQ_TC_PROBES.  Bit 3's runtime test stays: it sits between
+    // the unrolled chunk iterations of the scan, and without it ptxas schedules TMEM loads
+    // across chunks and spills at the 128-register cap
+    probe &= 8;
 #endif
     if (probe & 16) best_out = nullptr;
     constexpr int kStampItems = 2048;

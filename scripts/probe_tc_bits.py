@@ -1,4 +1,5 @@
-"""Time the tensor-core encode under CSPQ_TC_PROBE timing probes (debug only:
+"""Time the tensor-core encode under CSPQ_TC_PROBE timing probes (debug only: needs a build
+with -DCSPQ_TC_PROBES, e.g. NVFLAGS=-DCSPQ_TC_PROBES scripts/ab_build.sh wt p and CSPQ_LIB_PATH=build/ab/p/libcspq_b200.so;
 most probe bits produce garbage codes).  argv: config, comma list of probes."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -1,3 +1,4 @@
+# needs a -DCSPQ_TC_PROBES -DCSPQ_TC_STAMPS build (scripts/ab_build.sh, CSPQ_LIB_PATH)
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["CSPQ_TC_PROBE"] = sys.argv[1] if len(sys.argv) > 1 else "16"
