@@ -94,18 +94,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 }
 // bounded wait: a lost arrival traps (error) instead of hanging the device
 constexpr uint32_t kSuspendNs = 1000000;
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, bool spin = false) {
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
     long long t0 = 0;
-    if (spin) {  // (experiment) poll without suspending
-        for (long long i = 0;; ++i) {
-            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                         : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-            if (done) return;
-            if (i == 0) t0 = clock64();
-            else if ((i & 1023) == 0 && clock64() - t0 > 20000000000ll) __trap();
-        }
-    }
     for (bool first = true;; first = false) {
         // suspend (woken by the phase flip) instead of busy polling: spinning warps steal
         // issue slots from the epilogue warps that share their SM sub-partition
@@ -305,15 +296,15 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             const int64_t t0 = g * gs, tn = (ntiles - t0 < gs) ? (ntiles - t0) : gs;
             for (int j = 0; j < m; ++j, ++jt) {
                 const int jb = jt & 1;
-                mbar_wait(&H->b_full[jb], (jt >> 1) & 1, probe & 256);
+                mbar_wait(&H->b_full[jb], (jt >> 1) & 1);
                 for (int t = 0; t < tn; ++t, ++it) {
                     const int as = it % kNA, tb = it & 1;
-                    mbar_wait(&H->a_full[as], (it / kNA) & 1, probe & 256);
+                    mbar_wait(&H->a_full[as], (it / kNA) & 1);
                     if (stamp && lane == 0 && it < kStampItems) stamp[it * 8 + 0] = clock64();
                     const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
                     for (int c = 0; c < kNC; ++c) {
                         // chunk c of buffer tb drained by the scan of item it - 2
-                        if (it >= 2) mbar_wait(&H->t_empty[(it - 2) & 3][c], ((it - 2) >> 2) & 1, probe & 256);
+                        if (it >= 2) mbar_wait(&H->t_empty[(it - 2) & 3][c], ((it - 2) >> 2) & 1);
                         if (stamp && lane == 0 && c == 0 && it < kStampItems) stamp[it * 8 + 1] = clock64();
                         tc_fence_after();
                         const uint32_t bc = b0 + (uint32_t)(c * (kCW / 8) * S::kRowGroupBytes);  // centroids c kCW ..
@@ -341,7 +332,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
                 for (int j = 0; j < m; ++j, ++jt) {
                     const int jb = jt & 1;
-                    mbar_wait(&H->b_empty[jb], ((jt >> 1) & 1) ^ 1, probe & 1024);
+                    mbar_wait(&H->b_empty[jb], ((jt >> 1) & 1) ^ 1);
                     mbar_arrive_expect_tx(&H->b_full[jb], S::kBBytes + L::kCFloats * 4);
                     bulk_g2s(sB + jb * S::kBBytes, img + (int64_t)j * S::kBBytes, S::kBBytes, &H->b_full[jb]);
                     float *cdst = sC + jb * L::kCFloats;
@@ -462,7 +453,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 constexpr int kLdPerChunk = kCW / 64;
                 const int c = ch / kLdPerChunk;
                 if (ch % kLdPerChunk == 0) {
-                    mbar_wait(&H->t_full[it & 3][c], (it >> 2) & 1, probe & 512);
+                    mbar_wait(&H->t_full[it & 3][c], (it >> 2) & 1);
                     if (stamp && r == 0 && ch == 0 && it < kStampItems) stamp[it * 8 + 5] = clock64();
                     tc_fence_after();
                 }
