@@ -439,43 +439,64 @@ tc_settle_kernel(const float *__restrict__ P, int64_t n, int k, const double *__
     if (!state[j]) return;
     // the subspace's float64 codebook and norms in shared memory (k = 256: 8-16 KB + 2 KB);
     // every point gathers one centroid from it
-    __shared__ double sC[256 * SUBC], scn[256];
-    for (int q = threadIdx.x; q < k * SUBC; q += blockDim.x) sC[q] = C64[(int64_t)j * k * SUBC + q];
+    // (centroid stride SUBC + 1 doubles: random per-lane centroids spread over 16 bank pairs
+    // instead of 2 -- a 16-way conflict with the dense layout)
+    constexpr int kCS = SUBC + 1;
+    __shared__ double sC[256 * kCS], scn[256];
+    for (int q = threadIdx.x; q < k * SUBC; q += blockDim.x) sC[(q / SUBC) * kCS + q % SUBC] = C64[(int64_t)j * k * SUBC + q];
     for (int q = threadIdx.x; q < k; q += blockDim.x) scn[q] = cn_g[(int64_t)j * k + q];
     __syncthreads();
     const double *Cj = sC;
     const double *cnj = scn;
-    for (int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t ji = (int64_t)j * n + i;
-        double x[SUBC];
+    auto dist = [&](const double (&x)[SUBC], int l) {
+        const double *c = Cj + l * kCS;
+        double dot = 0.0;
 #pragma unroll
-        for (int t = 0; t < SUBC; ++t) x[t] = (double)P[ji * SUBC + t];
-        int bi;
-        double best;
-        auto dist = [&](int l) {
-            const double *c = Cj + (int64_t)l * SUBC;
-            double dot = 0.0;
+        for (int t = 0; t < SUBC; ++t) dot = __fma_rn(x[t], c[t], dot);
+        return __fma_rn(-2.0, dot, cnj[l]);
+    };
+    // two points per thread per step (independent loads in flight); x with 16-byte loads
+    constexpr int kPP = 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kPP;
+    for (int64_t i0 = b + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kPP; i0 < e; i0 += stride) {
+        double x[kPP][SUBC];
+        int bi[kPP];
+        bool fl[kPP], ok[kPP];
 #pragma unroll
-            for (int t = 0; t < SUBC; ++t) dot = __fma_rn(x[t], c[t], dot);
-            return __fma_rn(-2.0, dot, cnj[l]);
-        };
-        if (flags[ji]) {  // full float64 scan, first index on ties (assign_kernel's order)
-            best = 0.0;
-            bi = 0;
-            for (int l = 0; l < k; ++l) {
-                const double d1 = dist(l);
-                if (l == 0 || d1 < best) { best = d1; bi = l; }
+        for (int p = 0; p < kPP; ++p) {
+            ok[p] = i0 + p < e;
+            const int64_t ji = (int64_t)j * n + (ok[p] ? i0 + p : i0);
+            const float4 *xp = reinterpret_cast<const float4 *>(P + ji * SUBC);
+#pragma unroll
+            for (int q = 0; q < SUBC / 4; ++q) {
+                const float4 v = xp[q];
+                x[p][4 * q] = v.x; x[p][4 * q + 1] = v.y; x[p][4 * q + 2] = v.z; x[p][4 * q + 3] = v.w;
             }
-        } else {
-            bi = codes[ji];
-            best = dist(bi);
+            bi[p] = codes[ji];
+            fl[p] = flags[ji] != 0;
         }
-        double xx = 0.0;
 #pragma unroll
-        for (int t = 0; t < SUBC; ++t) xx = __dadd_rn(xx, __dmul_rn(x[t], x[t]));
-        const double v = __dadd_rn(best, xx);
-        assign[ji] = bi;
-        sq[ji] = (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(v, 0.0)
+        for (int p = 0; p < kPP; ++p) {
+            if (!ok[p]) break;
+            const int64_t ji = (int64_t)j * n + i0 + p;
+            double best;
+            if (fl[p]) {  // full float64 scan, first index on ties (assign_kernel's order)
+                best = 0.0;
+                bi[p] = 0;
+                for (int l = 0; l < k; ++l) {
+                    const double d1 = dist(x[p], l);
+                    if (l == 0 || d1 < best) { best = d1; bi[p] = l; }
+                }
+            } else {
+                best = dist(x[p], bi[p]);
+            }
+            double xx = 0.0;
+#pragma unroll
+            for (int t = 0; t < SUBC; ++t) xx = __dadd_rn(xx, __dmul_rn(x[p][t], x[p][t]));
+            const double v = __dadd_rn(best, xx);
+            assign[ji] = bi[p];
+            sq[ji] = (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(v, 0.0)
+        }
     }
 }
 
@@ -583,12 +604,23 @@ __global__ void sums_kernel(const TP *__restrict__ P, int64_t n, int m, int k, i
     const TP *Pj = P + ((int64_t)j * n + b) * sub + t;
     double s = 0.0;
     int32_t p = 0;
-    for (; p + 8 <= cc; p += 8) {
-        TP v[8];
+    // 16 gathers in flight per step; the next step's indices are loaded before this step's sum
+    constexpr int kB = 16;
+    int32_t idx[kB];
+    if (cc >= kB) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = Pj[(int64_t)pp[p + q] * sub];
+        for (int q = 0; q < kB; ++q) idx[q] = pp[q];
+    }
+    for (; p + kB <= cc; p += kB) {
+        TP v[kB];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s = __dadd_rn(s, (double)v[q]);
+        for (int q = 0; q < kB; ++q) v[q] = Pj[(int64_t)idx[q] * sub];
+        if (p + 2 * kB <= cc) {
+#pragma unroll
+            for (int q = 0; q < kB; ++q) idx[q] = pp[p + kB + q];
+        }
+#pragma unroll
+        for (int q = 0; q < kB; ++q) s = __dadd_rn(s, (double)v[q]);
     }
     for (; p < cc; ++p) s = __dadd_rn(s, (double)Pj[(int64_t)pp[p] * sub]);
     sums[g] = s;
@@ -910,7 +942,7 @@ static int assign_tc(const float *P, int64_t n, int m, int sub, int k, const dou
                            flags + b, nullptr, st)))
         return rc;
     // ~8 CTAs per SM in total: each CTA stages its subspace's codebook once for many points
-    dim3 grid((unsigned)grid_for(e - b, 256, std::max<int64_t>(1, 148 * 8 / m)), (unsigned)m);
+    dim3 grid((unsigned)grid_for((e - b + 1) / 2, 256, std::max<int64_t>(1, 148 * 8 / m)), (unsigned)m);
     if (sub == 8) tc_settle_kernel<8><<<grid, 256, 0, st>>>(P, n, k, C64, cn, state, b, e, codes, flags, assign, sq);
     else tc_settle_kernel<4><<<grid, 256, 0, st>>>(P, n, k, C64, cn, state, b, e, codes, flags, assign, sq);
     CSPQ_LAUNCH_CHECK();
