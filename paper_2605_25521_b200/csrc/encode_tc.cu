@@ -639,8 +639,12 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const flo
     const size_t smem = TcSmem<SUB, TIn>::total(m);
     CSPQ_REQUIRE(smem <= 227 * 1024, CSPQ_E_CONFIG, "too many subspaces (%d) for the tensor-core kernel", m);
     CSPQ_REQUIRE((n + kTM - 1) / kTM < ((int64_t)1 << 31), CSPQ_E_CONFIG, "too many rows (%lld) for one launch", (long long)n);
-    const char *pe = getenv("CSPQ_TC_PROBE");  // debug timing knob (instrumented variant), see the kernel
+#ifdef CSPQ_TC_PROBES
+    const char *pe = getenv("CSPQ_TC_PROBE");  // debug timing knob of the instrumented build, see the kernel
     const int probe = pe ? atoi(pe) : 0;
+#else
+    const int probe = 0;  // (a production build never reads the knob: probe bits change codes)
+#endif
     auto kern = encode_tc_kernel<SUB, TIn>;
     CSPQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 148;
