@@ -352,14 +352,16 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         const int r = 32 * q + lane;
         float *scratch = sScr + ((size_t)e * kTM + r) * kScrW;  // this thread's 32 block minima
         constexpr float kE = (float)((4.0 / 4194304.0 + S::kSteps / 4194304.0 * (1.0 + 1.0 / 1024.0) + (SUB + 1) / 16777216.0) * 1.01);
-        auto ring = [&](uint32_t item) -> unsigned char * {  // x slot of one of the group's items
-            return sX + ((size_t)e * kRing + (item / kGroups) % kRing) * L::kXBytes + r * SUB * sizeof(TIn);
+        // the group's x ring: owned item k (item e + kGroups k) lives in slot k % kRing
+        static_assert(kRing == kPD + 1, "slot rotation below assumes kRing == kPD + 1");
+        auto ring = [&](int slot) -> unsigned char * {
+            return sX + ((size_t)e * kRing + slot) * L::kXBytes + r * SUB * sizeof(TIn);
         };
-        auto prefetch = [&](const ItemIter &pi, uint32_t item) {
+        auto prefetch = [&](const ItemIter &pi, int slot) {
             const int64_t row = pi.tile() * kTM + r;
             const bool ok = pi.valid() && row < n;
             const TIn *src = X + (ok ? row * xs + (int64_t)pi.j * xjs : 0);
-            unsigned char *dst = ring(item);
+            unsigned char *dst = ring(slot);
             constexpr int bytes = SUB * (int)sizeof(TIn);
             if constexpr (bytes == 32) {
                 cp_async16(dst, src, ok ? 16 : 0);
@@ -373,9 +375,11 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             }
             cp_async_commit();
         };
-        // A row of item `item` (stage item % kNA) from the staged x; returns ||x|| rounded up
-        auto convert = [&](uint32_t item) -> float {
-            const TIn *xr = reinterpret_cast<const TIn *>(ring(item));
+        // A row of the group's next item (A stage e: the group's items are all == e mod kNA) from
+        // the staged x of ring slot `slot`; returns ||x|| rounded up
+        static_assert(kNA == kGroups, "A stage = item % kNA = the group index");
+        auto convert = [&](int slot) -> float {
+            const TIn *xr = reinterpret_cast<const TIn *>(ring(slot));
             float x[SUB];
             if constexpr (sizeof(TIn) == 4) {
 #pragma unroll
@@ -399,7 +403,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 ss = __fmaf_rn(x[tt], x[tt], ss);
             }
             if (!(probe & 4)) {
-                unsigned char *rowp = sA + (item % kNA) * S::kABytes + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16;
+                unsigned char *rowp = sA + e * S::kABytes + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16;
                 auto st = [&](int c, float a0, float a1, float a2, float a3) {
                     *reinterpret_cast<float4 *>(rowp + c * 128) = make_float4(a0, a1, a2, a3);
                 };
@@ -414,7 +418,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 }
             }
             fence_proxy_async();
-            mbar_arrive(&H->a_full[item % kNA]);
+            mbar_arrive(&H->a_full[e]);
             return __fsqrt_ru(ss) * 1.000001f;
         };
         // b_empty[p & 1] phase p >> 1 belongs to pair p.  A group that owns no item of
@@ -430,17 +434,23 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         ItemIter ii(blockIdx.x, (int)ngroups, (int)ntiles, m, gs);
         ii.advance(e, gridDim.x);
         ItemIter ip = ii;
-        uint32_t ipi = e;
-        for (int d = 0; d < kPD; ++d, ipi += kGroups, ip.advance(kGroups, gridDim.x)) prefetch(ip, ipi);
+        for (int d = 0; d < kPD; ++d, ip.advance(kGroups, gridDim.x)) prefetch(ip, d);
         float norm_cur = 0.f;
-        if (ii.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(e); }
+        if (ii.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(0); }
         ItemIter ic = ii;
         ic.advance(kGroups, gridDim.x);
-        uint32_t ici = e + kGroups;
         uint32_t rel = 0;  // pairs below rel are released by this thread
+        // ring slots of the current item, the next one (A conversion) and the prefetched one
+        int s_cur = 0, s_next = 1, s_pf = 2;
+        auto rotate = [&] {  // the current item's slot becomes the next prefetch target
+            const int s_old = s_cur;
+            s_cur = s_next;
+            s_next = s_pf;
+            s_pf = s_old;
+        };
 
         for (uint32_t it = e; ii.valid(); it += kGroups, ii.advance(kGroups, gridDim.x), ic.advance(kGroups, gridDim.x),
-                                          ip.advance(kGroups, gridDim.x), ici += kGroups, ipi += kGroups) {
+                                          ip.advance(kGroups, gridDim.x), rotate()) {
             for (; rel < ii.jt; ++rel) release_pair(rel);  // done with those pairs' sC
             const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
@@ -493,11 +503,11 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 6] = clock64();
             // the group's next item: stage its x prefetch and write its A operand now, so
             // its MMA can start as soon as the other group's item is done
-            if (!(probe & 32)) prefetch(ip, ipi);  // (an empty group keeps the wait count uniform)
+            if (!(probe & 32)) prefetch(ip, s_pf);  // (an empty group keeps the wait count uniform)
             float norm_next = 0.f;
             if (ic.valid()) {
                 if (!(probe & 32)) cp_async_wait<kPD - 1>();
-                norm_next = convert(ici);
+                norm_next = convert(s_next);
             }
             const float xnorm = norm_cur;
             norm_cur = norm_next;
@@ -559,7 +569,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 while (mask) {
                     const int src = __ffs(mask) - 1;
                     mask &= mask - 1;
-                    const TIn *xr = reinterpret_cast<const TIn *>(sX + ((size_t)e * kRing + (it / kGroups) % kRing) * L::kXBytes) +
+                    const TIn *xr = reinterpret_cast<const TIn *>(sX + ((size_t)e * kRing + s_cur) * L::kXBytes) +
                                     (32 * q + src) * SUB;
                     float xv[SUB];
 #pragma unroll
