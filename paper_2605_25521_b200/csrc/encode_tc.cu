@@ -224,7 +224,9 @@ struct TcSmem {
 };
 
 // ------------------------------------------------------------------ the kernel
-template <int SUB, typename TIn>
+// kMark: mark mode (flags written, no fix-up; the Lloyd screen) -- a template so the encode
+// path carries no per-item test of it
+template <int SUB, typename TIn, bool kMark>
 __global__ void __launch_bounds__(kThreads, 1)
 encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_t xjs, const float *__restrict__ CB,
                  const float *__restrict__ Bv, const float *__restrict__ guard, const uint8_t *__restrict__ img,
@@ -554,12 +556,12 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             const bool flag = (row < n) && !(ncf == 1.0f && nbf == 1.0f);
             // exact warp-cooperative re-encode of flagged rows (x and the fp32 codebook from
             // shared memory: the item's x slot stays valid until kPD more owned items)
-            if (flags) {  // mark mode (Lloyd screening): flagged rows are settled by the caller
+            if constexpr (kMark) {  // mark mode (Lloyd screening): flagged rows are settled by the caller
                 if (row < n) flags[row * cs + j * cjs] = flag ? 1 : 0;
                 const unsigned fm = __ballot_sync(0xffffffffu, flag);
                 if (lane == 0 && fm) atomicAdd(&g_tc_flagged, (unsigned long long)__popc(fm));
             }
-            unsigned mask = __ballot_sync(0xffffffffu, flag && !(probe & 15) && !flags);
+            unsigned mask = kMark ? 0u : __ballot_sync(0xffffffffu, flag && !(probe & 15));
             if (mask) {
                 // acquire the bulk copies of this pair (the buffer cannot advance past this
                 // pair until every epilogue thread has arrived on b_empty)
@@ -655,7 +657,7 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const flo
 #else
     const int probe = 0;  // (a production build never reads the knob: probe bits change codes)
 #endif
-    auto kern = encode_tc_kernel<SUB, TIn>;
+    auto kern = flags ? encode_tc_kernel<SUB, TIn, true> : encode_tc_kernel<SUB, TIn, false>;
     CSPQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
