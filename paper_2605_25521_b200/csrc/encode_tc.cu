@@ -224,9 +224,9 @@ struct TcSmem {
 };
 
 // ------------------------------------------------------------------ the kernel
-// kMark: mark mode (flags written, no fix-up; the Lloyd screen) -- a template so the encode
-// path carries no per-item test of it
-template <int SUB, typename TIn, bool kMark>
+// kMark: mark mode (flags written, no fix-up; the Lloyd screen); kBest: the winning scores are
+// written to best_out (tests) -- templates, so the encode path carries no per-item test of them
+template <int SUB, typename TIn, bool kMark, bool kBest>
 __global__ void __launch_bounds__(kThreads, 1)
 encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_t xjs, const float *__restrict__ CB,
                  const float *__restrict__ Bv, const float *__restrict__ guard, const uint8_t *__restrict__ img,
@@ -597,7 +597,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             }
             if (row < n) {
                 if (!(probe & 64)) codes[row * cs + j * cjs] = (uint8_t)code;
-                if (best_out) best_out[row * m + j] = m1;
+                if constexpr (kBest) {
+                    if (!stamp) best_out[row * m + j] = m1;  // (a stamp run borrows best_out)
+                }
             }
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 7] = clock64();
         }
@@ -657,7 +659,8 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const flo
 #else
     const int probe = 0;  // (a production build never reads the knob: probe bits change codes)
 #endif
-    auto kern = flags ? encode_tc_kernel<SUB, TIn, true> : encode_tc_kernel<SUB, TIn, false>;
+    auto kern = flags ? (best ? encode_tc_kernel<SUB, TIn, true, true> : encode_tc_kernel<SUB, TIn, true, false>)
+                      : (best ? encode_tc_kernel<SUB, TIn, false, true> : encode_tc_kernel<SUB, TIn, false, false>);
     CSPQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
