@@ -213,17 +213,31 @@ def _sample(points: np.ndarray, cap: int | None, rng: np.random.Generator) -> np
 
 def _train_many(subspace_points, cfg: TrainConfig, rngs, labels):
     """Sample, validate, seed and train a list of subspaces together."""
-    sampled = []
-    for pts, rng, j in zip(subspace_points, rngs, labels):
-        try:
-            s = _sample(pts, cfg.resolved_cap(), rng)
-            s64 = np.asarray(s, dtype=np.float64)
-            _validate_points(s64, cfg.k)
-        except (TrainingError, DataError) as exc:
-            raise type(exc)(f"subspace {j}: {exc}") from None
-        sampled.append(s64)
-    # stack (and exactness-check) once, move to the GPU once; both stages read the tensor
-    P, _ = _stack_points(sampled)
+    samples = [_sample(pts, cfg.resolved_cap(), rng) for pts, rng in zip(subspace_points, rngs)]
+    P = None
+    if all(s.dtype == np.float32 for s in samples) and len({s.shape for s in samples}) == 1:
+        # float32 data (every configuration): float64(x) is exact and injective there, so the
+        # count / distinct checks give the reference's answers on the float32 rows and the stack
+        # needs no float64 round trip (~0.7 s of host time for c3-shaped data)
+        P32 = np.ascontiguousarray(np.stack(samples))
+        if np.isfinite(P32).all():
+            for s, j in zip(P32, labels):
+                try:
+                    _validate_points(s, cfg.k)
+                except (TrainingError, DataError) as exc:
+                    raise type(exc)(f"subspace {j}: {exc}") from None
+            P = P32
+    if P is None:
+        sampled = []
+        for s, j in zip(samples, labels):
+            try:
+                s64 = np.asarray(s, dtype=np.float64)
+                _validate_points(s64, cfg.k)
+            except (TrainingError, DataError) as exc:
+                raise type(exc)(f"subspace {j}: {exc}") from None
+            sampled.append(s64)
+        P, _ = _stack_points(sampled)
+    # move to the GPU once; both stages read the tensor
     dev = device()
     Pd = to_device(P, dev)
     init = kmeanspp_init_batched(Pd, cfg.k, rngs, dev)
