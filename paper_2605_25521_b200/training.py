@@ -15,6 +15,7 @@ the seeding draws, and input validation.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -213,7 +214,16 @@ def _sample(points: np.ndarray, cap: int | None, rng: np.random.Generator) -> np
 
 def _train_many(subspace_points, cfg: TrainConfig, rngs, labels):
     """Sample, validate, seed and train a list of subspaces together."""
-    samples = [_sample(pts, cfg.resolved_cap(), rng) for pts, rng in zip(subspace_points, rngs)]
+    # every subspace has its own generator, so the draws and gathers run on host threads
+    # (numpy releases the GIL in both) with exactly the reference's per-stream draw order
+    cap = cfg.resolved_cap()
+    jobs = list(zip(subspace_points, rngs))
+    if len(jobs) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(min(len(jobs), os.cpu_count() or 1)) as ex:
+            samples = list(ex.map(lambda pr: _sample(pr[0], cap, pr[1]), jobs))
+    else:
+        samples = [_sample(p, cap, r) for p, r in jobs]
     P = None
     if all(s.dtype == np.float32 for s in samples) and len({s.shape for s in samples}) == 1:
         # float32 data (every configuration): float64(x) is exact and injective there, so the
