@@ -399,9 +399,14 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             float xh[SUB], xl[SUB], ss = 0.f;
 #pragma unroll
             for (int tt = 0; tt < SUB; ++tt) {
-                const float c = __fmul_rn(x[tt], 8193.0f);
-                xh[tt] = __fsub_rn(c, __fsub_rn(c, x[tt]));
-                xl[tt] = __fsub_rn(x[tt], xh[tt]);
+                if constexpr (sizeof(TIn) == 1) {  // bytes are exact in tf32: no split
+                    xh[tt] = x[tt];
+                    xl[tt] = 0.f;
+                } else {
+                    const float c = __fmul_rn(x[tt], 8193.0f);
+                    xh[tt] = __fsub_rn(c, __fsub_rn(c, x[tt]));
+                    xl[tt] = __fsub_rn(x[tt], xh[tt]);
+                }
                 ss = __fmaf_rn(x[tt], x[tt], ss);
             }
             if (!(probe & 4)) {
