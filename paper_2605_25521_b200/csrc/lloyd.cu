@@ -801,23 +801,20 @@ __global__ void kpp_dist_kernel(const TP *__restrict__ P, int64_t n, int sub, co
 }
 
 // p = d2 / total (np: p = d2 / total)
-__global__ void kpp_div_kernel(const double *__restrict__ d2, int64_t n, const double *__restrict__ total,
-                               const int32_t *__restrict__ status, double *__restrict__ pp) {
-    const int j = blockIdx.y;
-    if (status[j]) return;
-    const double tot = total[j];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        pp[(int64_t)j * n + i] = __ddiv_rn(d2[(int64_t)j * n + i], tot);
-}
-
-// rng.choice(n, p=p): cdf = cumsum(p) (sequential); cdf /= cdf[-1];
-// idx = searchsorted(cdf, u, 'right').  One CTA per subspace: chunks of the
-// probabilities are staged in shared memory with coalesced loads, thread 0
-// runs numpy's sequential chain over the chunk (in shared memory, loads issued
-// ahead of the dependent adds), the CTA writes the chunk back; then a binary
-// search over the normalised (monotone) cdf.
+// rng.choice(n, p=p): p = d2 / total; cdf = cumsum(p) (sequential); cdf /= cdf[-1];
+// idx = searchsorted(cdf, u, 'right').  One CTA per subspace: chunks of the probabilities are
+// computed into shared memory (coalesced loads of d2, the same IEEE division as numpy's p) and
+// thread 0 runs numpy's sequential chain over
+// them (loads issued ahead of the dependent adds).  Only every kSeg-th running sum is kept
+// (written over already-consumed probabilities); the search finds the segment among those, then
+// re-runs that segment's chain from its start -- the same operations in the same order -- to
+// find the index.  (The cdf is
+// monotone, so the first index whose normalised cdf exceeds u lies in the first segment whose
+// end does.)
 constexpr int kKppChunk = 4096;
-__global__ void __launch_bounds__(256) kpp_choose_kernel(double *__restrict__ pp, int64_t n, int m, int k, int c,
+constexpr int kSeg = 64;
+__global__ void __launch_bounds__(256) kpp_choose_kernel(double *__restrict__ pp, const double *__restrict__ d2,
+                                                         int64_t n, int m, int k, int c,
                                                          const double *__restrict__ total, const double *__restrict__ u,
                                                          int32_t *__restrict__ status, const void *P, int pf64, int sub,
                                                          double *__restrict__ C64) {
@@ -829,38 +826,52 @@ __global__ void __launch_bounds__(256) kpp_choose_kernel(double *__restrict__ pp
         if (threadIdx.x == 0) status[j] = 2;
         return;
     }
-    double *cdf = pp + (int64_t)j * n;
+    double *cdf = pp + (int64_t)j * n;  // segment-end sums (cdf[s] = sum through s*kSeg+kSeg-1)
+    const double tot = total[j];
+    const double *dj = d2 + (int64_t)j * n;
     if (threadIdx.x == 0) s_run = 0.0;
     for (int64_t c0 = 0; c0 < n; c0 += kKppChunk) {
         const int len = (int)(n - c0 < kKppChunk ? n - c0 : kKppChunk);
-        for (int i = threadIdx.x; i < len; i += blockDim.x) buf[i] = cdf[c0 + i];
+        for (int i = threadIdx.x; i < len; i += blockDim.x) buf[i] = __ddiv_rn(dj[c0 + i], tot);  // p = d2 / total
         __syncthreads();
         if (threadIdx.x == 0) {
             double run = s_run;
             int i = 0;
-            for (; i + 8 <= len; i += 8) {
-                double v[8];
+            for (; i + 16 <= len; i += 16) {
+                double v[16];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) v[q] = buf[i + q];
+                for (int q = 0; q < 16; ++q) v[q] = buf[i + q];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) { run = __dadd_rn(run, v[q]); buf[i + q] = run; }
+                for (int q = 0; q < 16; ++q) run = __dadd_rn(run, v[q]);
+                // kKppChunk and 16 are multiples of... 16 | kSeg: a segment ends on this step's last element
+                if (((c0 + i + 16) % kSeg) == 0) cdf[(c0 + i + 16) / kSeg - 1] = run;
             }
-            for (; i < len; ++i) { run = __dadd_rn(run, buf[i]); buf[i] = run; }
+            for (; i < len; ++i) {
+                run = __dadd_rn(run, buf[i]);
+                if (((c0 + i + 1) % kSeg) == 0) cdf[(c0 + i + 1) / kSeg - 1] = run;
+            }
             s_run = run;
         }
-        __syncthreads();
-        for (int i = threadIdx.x; i < len; i += blockDim.x) cdf[c0 + i] = buf[i];
         __syncthreads();
     }
     if (threadIdx.x != 0) return;
     const double last = s_run;
     const double uu = u[(int64_t)j * (k - 1) + (c - 1)];
-    int64_t lo = 0, hi = n;  // first i with cdf[i]/last > uu
+    // segments [s kSeg, (s + 1) kSeg); the last one may be partial and has no stored end
+    const int64_t nseg = (n + kSeg - 1) / kSeg, nfull = n / kSeg;
+    int64_t lo = 0, hi = nfull;  // first full segment whose end exceeds u (or nfull)
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if (__ddiv_rn(cdf[mid], last) > uu) hi = mid; else lo = mid + 1;
     }
-    int64_t idx = lo < n ? lo : n - 1;  // u < 1 and cdf[-1]/last == 1 keep lo < n
+    const int64_t seg = lo < nseg ? lo : nseg - 1;
+    double run = seg > 0 ? cdf[seg - 1] : 0.0;
+    const int64_t e = (seg + 1) * kSeg < n ? (seg + 1) * kSeg : n;
+    int64_t idx = e - 1;  // u < 1 and cdf[-1]/last == 1 find an index before the end
+    for (int64_t i = seg * kSeg; i < e; ++i) {
+        run = __dadd_rn(run, __ddiv_rn(dj[i], tot));
+        if (__ddiv_rn(run, last) > uu) { idx = i; break; }
+    }
     double *dst = C64 + ((int64_t)j * k + c) * sub;
     for (int t = 0; t < sub; ++t)
         dst[t] = pf64 ? reinterpret_cast<const double *>(P)[((int64_t)j * n + idx) * sub + t]
@@ -1115,9 +1126,7 @@ int kmeanspp(const void *P, int pf64, int64_t n, int m, int sub, int k, const in
         for (int c = 1; c < k; ++c) {
             // status doubles as the "active" mask of pairwise_obj: 0 -> active
             if ((rc = pairwise_obj(d2, n, 0, n, m, nullptr, ws, L, total, st))) return rc;
-            kpp_div_kernel<<<g, 256, 0, st>>>(d2, n, total, status, pp);
-            CSPQ_LAUNCH_CHECK();
-            kpp_choose_kernel<<<m, 256, 0, st>>>(pp, n, m, k, c, total, u, status, P, pf64, sub, C64);
+            kpp_choose_kernel<<<m, 256, 0, st>>>(pp, d2, n, m, k, c, total, u, status, P, pf64, sub, C64);
             CSPQ_LAUNCH_CHECK();
             kpp_dist_kernel<TP><<<g, 256, 0, st>>>(Pt, n, sub, C64, k, c, status, d2, 0);
             CSPQ_LAUNCH_CHECK();
