@@ -42,9 +42,9 @@ def parse():
     p.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     p.add_argument("--mode", default="auto", choices=["auto", "exact", "guarded"])
     p.add_argument("--e2e-rows", type=int, default=0,
-                   help="rows per rank through the host API (0 = 2M, or the whole config for c5)")
+                   help="rows per rank through the host API (0 = max(2M, 6 GB of rows), or the whole config for c5)")
     p.add_argument("--streams", type=int, default=0, help="host pipeline streams (0 = 3, or 6 for c5)")
-    p.add_argument("--e2e-batch", type=int, default=0, help="host pipeline batch rows (0 = 131072, or 4096 for c5)")
+    p.add_argument("--e2e-batch", type=int, default=0, help="host pipeline batch rows (0 = max(131072, 256 MB of rows), or 4096 for c5)")
     p.add_argument("--train", choices=["auto", "sharded", "rank0"], default="auto",
                    help="codebook training: row-sharded Lloyd with one all-reduce per iteration (auto: when N > 1), "
                         "or the fused single-GPU cspq_lloyd_train on rank 0 + broadcast")
@@ -268,8 +268,12 @@ def main():
     if not args.no_e2e:
         # c5 is the streaming config: the reference's 4096-row batches from pinned host memory,
         # whole dataset per step, with per-batch H2D -> encode -> D2H latency from device events
-        ne = min(args.e2e_rows or (cfg.n if cfg.batch else 2_000_000), rows)
-        batch_rows = cfg.batch or args.e2e_batch or (1 << 17)  # 128K..1M rows all saturate PCIe (54-55 GB/s)
+        # sized in bytes, so short rows (c4: 128 B) get batches and samples as large as long ones:
+        # ~6 GB of rows per step and batches of >= 128K rows and >= 256 MB (c3: 2M rows, 128K-row
+        # batches -- 128K..1M rows all saturate PCIe at 54-55 GB/s; c4: 47M rows, 2M-row batches)
+        row_bytes = cfg.d * cfg.elem_bytes
+        ne = min(args.e2e_rows or (cfg.n if cfg.batch else max(2_000_000, (6 << 30) // row_bytes)), rows)
+        batch_rows = cfg.batch or args.e2e_batch or max(1 << 17, (256 << 20) // row_bytes)
         Xh = P.pinned_empty((ne, cfg.d), np.uint8 if cfg.dtype == "u8" else np.float32)
         Xh[:] = X[:ne].cpu().numpy()
         codes_h = P.pinned_empty((ne, cfg.m), np.uint8)
