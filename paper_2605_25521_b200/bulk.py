@@ -41,8 +41,10 @@ class ExecutionPlan:
     give the oracle's codes; "tensor" = the tcgen05 kernel, "guarded" = the
     FFMA kernel, "exact" = strict fp32 chains, "auto" = tensor where the
     shape allows it, else guarded), ``batch_rows`` (rows per host<->device batch; None =
-    max(block_size, 65536)), ``streams`` (CUDA streams in that pipeline) and
-    ``device`` (CUDA ordinal; None = current)."""
+    max(block_size, 65536)), ``streams`` (CUDA streams in that pipeline),
+    ``device`` (CUDA ordinal; None = current) and ``devices`` (several ordinals: host rows
+    are split into contiguous ranges, one pipeline per GPU on its own PCIe link -- the
+    single-process counterpart of the reference's worker threads)."""
 
     order: str = CHUNK_MAJOR
     block_size: int = 4096
@@ -53,6 +55,7 @@ class ExecutionPlan:
     batch_rows: int | None = None
     streams: int = 3
     device: int | None = None
+    devices: tuple | None = None
 
     def __post_init__(self):
         if self.order not in (CHUNK_MAJOR, VECTOR_MAJOR):
@@ -69,6 +72,11 @@ class ExecutionPlan:
             raise ConfigError(f"batch_rows must be >= 1, got {self.batch_rows}")
         if not 1 <= self.streams <= 16:
             raise ConfigError(f"streams must be in [1, 16], got {self.streams}")
+        if self.devices is not None:
+            devs = tuple(self.devices)
+            if not devs or any(not isinstance(d, (int, np.integer)) or d < 0 for d in devs):
+                raise ConfigError(f"devices must be a non-empty sequence of CUDA ordinals, got {self.devices!r}")
+            object.__setattr__(self, "devices", tuple(int(d) for d in devs))
 
     def resolved_w(self) -> int:
         return self.w if self.w is not None else native_lane_width()
@@ -246,12 +254,34 @@ def encode_dataset_device(X, codebooks, plan: ExecutionPlan | None = None, *,
     return out
 
 
+def _encode_host_multi(X, cbset, plan: ExecutionPlan, precomputed_bias: bool, out: np.ndarray) -> np.ndarray:
+    """plan.devices: contiguous row ranges, one host pipeline per GPU, run from host threads
+    (each C call releases the GIL).  Rows are independent, so the codes equal a single
+    device's (the reference's plan invariance, test_bulk.py:44-62)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from dataclasses import replace
+    devs = plan.devices
+    n = X.shape[0]
+    bounds = [n * i // len(devs) for i in range(len(devs) + 1)]
+    jobs = [(d, bounds[i], bounds[i + 1]) for i, d in enumerate(devs) if bounds[i + 1] > bounds[i]]
+
+    def run(job):
+        d, b, e = job
+        encode_dataset_host(X[b:e], cbset, replace(plan, device=d, devices=None), precomputed_bias=precomputed_bias,
+                            out=out[b:e])
+
+    with ThreadPoolExecutor(len(jobs)) as ex:
+        list(ex.map(run, jobs))  # (re-raises the first failure)
+    return out
+
+
 def encode_dataset_host(X: np.ndarray, codebooks, plan: ExecutionPlan | None = None, *,
                         precomputed_bias: bool = True, out: np.ndarray | None = None,
                         batch_ms: np.ndarray | None = None) -> np.ndarray:
     """Encode host rows through the C ABI's pipelined H2D -> encode -> D2H path
     (cspq_encode_host).  Pinned inputs/outputs (``pinned_empty``) are copied
-    directly; pageable ones are staged through a pinned ring."""
+    directly; pageable ones are staged through a pinned ring.  ``plan.devices``
+    spreads the rows over several GPUs (one pipeline each)."""
     N.require_cuda()
     plan = plan or ExecutionPlan()
     cbset = CodebookSet.from_codebooks(codebooks)
@@ -268,7 +298,11 @@ def encode_dataset_host(X: np.ndarray, codebooks, plan: ExecutionPlan | None = N
         return out
     if d != cbset.d:
         raise ConfigError(f"dataset dimensionality {d} does not match codebooks' d={cbset.d}")
-    dev = _device(plan.device)
+    if plan.devices is not None and len(plan.devices) > 1:
+        if batch_ms is not None:
+            raise ConfigError("batch_ms is per pipeline: not available with several devices")
+        return _encode_host_multi(X, cbset, plan, precomputed_bias, out)
+    dev = _device(plan.device if plan.devices is None else plan.devices[0])
     rm, bs, guard, vid = _variant_args(cbset, plan, precomputed_bias, dev)
     t = torch()
     t.cuda.current_stream(dev).synchronize()  # codebook upload visible to the pipeline streams

@@ -210,6 +210,29 @@ def test_plan_invariance(P, bulk_setup):
                     assert got.tobytes() == base.tobytes()
 
 
+def test_multi_device_split(P, oracle):
+    """ExecutionPlan(devices=...): host rows split into contiguous ranges, one pipeline per
+    device from host threads (the same GPU twice / three times here: the one-GPU box still
+    exercises the split, the threads and the per-range outputs); codes equal one device's
+    and the oracle's, for ragged sizes, pinned and pageable input, the tensor-core and SIMT
+    paths."""
+    rng = np.random.default_rng(8)
+    m, sub, k = 12, 8, 256
+    rm = rng.standard_normal((m, k, sub)).astype(np.float32)
+    cbs = [P.Codebook.from_rowmajor(j, rm[j]) for j in range(m)]
+    cs = P.CodebookSet.from_codebooks(cbs)
+    for n in (1, 5, 100_003):
+        X = rng.standard_normal((n, m * sub)).astype(np.float32)
+        want = oracle.encode(X, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM)
+        Xp = P.pinned_empty(X.shape, np.float32)
+        Xp[:] = X
+        for devs in ((0, 0), (0, 0, 0)):
+            for mode in ("auto", "guarded"):
+                plan = P.ExecutionPlan(devices=devs, mode=mode, batch_rows=16_384)
+                assert P.encode_dataset(X, cbs, plan).codes.tobytes() == want.tobytes(), (n, devs, mode)
+                assert P.encode_dataset_host(Xp, cbs, plan).tobytes() == want.tobytes(), (n, devs, mode)
+
+
 def test_empty_and_mismatch(P, bulk_setup):
     _, cbs = bulk_setup
     out = P.encode_dataset(np.empty((0, 12), np.float32), cbs, P.ExecutionPlan())

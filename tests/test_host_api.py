@@ -170,3 +170,11 @@ def test_encode_dataset_device_rejects_host_tensors_and_bad_outputs():
         P.encode_dataset_device(torch.zeros((4, 8)), cbs)
     with pytest.raises(P.ConfigError, match="CUDA tensor"):
         P.encode_dataset_device(np.zeros((4, 8), np.float32), cbs)
+
+
+def test_execution_plan_devices_validation():
+    assert P.ExecutionPlan(devices=[0, 1]).devices == (0, 1)
+    assert P.ExecutionPlan(devices=np.array([2, 3])).devices == (2, 3)
+    for bad in ([], [-1], [0.5], ["0"]):
+        with pytest.raises(P.ConfigError, match="devices"):
+            P.ExecutionPlan(devices=bad)
