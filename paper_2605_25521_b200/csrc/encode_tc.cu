@@ -182,28 +182,29 @@ struct TcSmemHdr {
     uint32_t tmem_base;
 };
 
-// walk of the (row group, subspace, tile) work items of one CTA (32-bit counters: the launch
-// checks ntiles < 2^31; tile() widens)
+// walk of the (row group, subspace, tile) work items of one CTA: the CTA owns the contiguous
+// range [p, p_end) of (row group, subspace) pairs, pair p = g * m + j (32-bit counters: the launch
+// checks ngroups * m < 2^31; tile() widens)
 struct ItemIter {
-    int g, ngroups, ntiles;
-    int j, t, m, tn, gs;  // gs: tiles per row group
-    uint32_t jt;  // (row group, subspace) pairs started before the current one
-    __device__ ItemIter(int g0, int ng, int nt, int m_, int gs_)
-        : g(g0), ngroups(ng), ntiles(nt), j(0), t(0), m(m_), tn(0), gs(gs_), jt(0) {
-        tn = g < ng ? min(nt - g * gs, gs) : 0;
+    int g, j, t, tn, p, p_end, m, gs, ntiles;
+    uint32_t jt;  // pairs walked before the current one
+    __device__ ItemIter(int p0, int p1, int m_, int gs_, int nt)
+        : g(p0 / m_), j(p0 % m_), t(0), tn(0), p(p0), p_end(p1), m(m_), gs(gs_), ntiles(nt), jt(0) {
+        tn = p < p_end ? min(ntiles - g * gs, gs) : 0;
     }
-    __device__ bool valid() const { return g < ngroups; }
+    __device__ bool valid() const { return p < p_end; }
     __device__ int64_t tile() const { return (int64_t)g * gs + t; }
     // k items ahead (jt counts every pair boundary crossed, as k single steps would)
-    __device__ void advance(int k, int stride) {
+    __device__ void advance(int k) {
         t += k;
-        while (g < ngroups && t >= tn) {
+        while (p < p_end && t >= tn) {
             t -= tn;
             ++jt;
+            ++p;
             if (++j >= m) {
                 j = 0;
-                g += stride;
-                tn = g < ngroups ? min(ntiles - g * gs, gs) : 0;
+                ++g;
+                tn = min(ntiles - g * gs, gs);
             }
         }
     }
@@ -263,6 +264,10 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (n + kTM - 1) / kTM;
     const int64_t ngroups = (ntiles + gs - 1) / gs;
+    // contiguous pair ranges balance the SMs at pair granularity (a whole row group per CTA
+    // left up to a row group's worth of items of imbalance: c1's 782 tiles)
+    const int64_t npairs = ngroups * m;
+    const int p_begin = (int)(npairs * blockIdx.x / gridDim.x), p_end = (int)(npairs * (blockIdx.x + 1) / gridDim.x);
 
     for (int i = threadIdx.x; i < 2 * m; i += kThreads) sGuard[i] = guard[i];
     if (threadIdx.x == 0) {
@@ -294,9 +299,10 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         // one elected lane issues: no per-thread -> uniform register waterfall around each MMA
         // (scripts/micro/umma_rate.cu: 676 vs 756 cycles from issue to completion of an item).
         uint32_t it = 0, jt = 0;
-        for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-            const int64_t t0 = g * gs, tn = (ntiles - t0 < gs) ? (ntiles - t0) : gs;
-            for (int j = 0; j < m; ++j, ++jt) {
+        for (int p = p_begin; p < p_end; ++p, ++jt) {
+            const int g = p / m;
+            const int64_t t0 = (int64_t)g * gs, tn = (ntiles - t0 < gs) ? (ntiles - t0) : gs;
+            {
                 const int jb = jt & 1;
                 mbar_wait(&H->b_full[jb], (jt >> 1) & 1);
                 for (int t = 0; t < tn; ++t, ++it) {
@@ -331,8 +337,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         // ---------------- codebook loader: tf32 image (MMA) + fp32 codebook (fix-up) ----------------
         if (lane == 0) {
             uint32_t jt = 0;
-            for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-                for (int j = 0; j < m; ++j, ++jt) {
+            for (int p = p_begin; p < p_end; ++p) {
+                {
+                    const int j = p % m;
                     const int jb = jt & 1;
                     mbar_wait(&H->b_empty[jb], ((jt >> 1) & 1) ^ 1);
                     mbar_arrive_expect_tx(&H->b_full[jb], S::kBBytes + L::kCFloats * 4);
@@ -340,6 +347,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                     float *cdst = sC + jb * L::kCFloats;
                     bulk_g2s(cdst, CB + (int64_t)j * kN * SUB, kN * SUB * 4, &H->b_full[jb]);
                     bulk_g2s(cdst + kN * SUB, Bv + (int64_t)j * kN, kN * 4, &H->b_full[jb]);
+                    ++jt;
                 }
             }
         }
@@ -438,14 +446,14 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 
         // The group walks its own items only (item e, e + kGroups, ...); ic / ip run kGroups
         // and kGroups kPD items ahead for the A conversion and the x prefetch.
-        ItemIter ii(blockIdx.x, (int)ngroups, (int)ntiles, m, gs);
-        ii.advance(e, gridDim.x);
+        ItemIter ii(p_begin, p_end, m, gs, (int)ntiles);
+        ii.advance(e);
         ItemIter ip = ii;
-        for (int d = 0; d < kPD; ++d, ip.advance(kGroups, gridDim.x)) prefetch(ip, d);
+        for (int d = 0; d < kPD; ++d, ip.advance(kGroups)) prefetch(ip, d);
         float norm_cur = 0.f;
         if (ii.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(0); }
         ItemIter ic = ii;
-        ic.advance(kGroups, gridDim.x);
+        ic.advance(kGroups);
         uint32_t rel = 0;  // pairs below rel are released by this thread
         // ring slots of the current item, the next one (A conversion) and the prefetched one
         int s_cur = 0, s_next = 1, s_pf = 2;
@@ -456,8 +464,8 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             s_pf = s_old;
         };
 
-        for (uint32_t it = e; ii.valid(); it += kGroups, ii.advance(kGroups, gridDim.x), ic.advance(kGroups, gridDim.x),
-                                          ip.advance(kGroups, gridDim.x), rotate()) {
+        for (uint32_t it = e; ii.valid(); it += kGroups, ii.advance(kGroups), ic.advance(kGroups), ip.advance(kGroups),
+                                          rotate()) {
             for (; rel < ii.jt; ++rel) release_pair(rel);  // done with those pairs' sC
             const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
@@ -671,19 +679,13 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const flo
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ntiles = (n + kTM - 1) / kTM;
-    // tiles per row group: minimise the busiest CTA's cost, tiles x (1 + 0.5 / gs) -- every
-    // (row group, subspace) pair reloads a 41 KB codebook image, measured ~ half a tile's
-    // time spread over the group's tiles (c1's 782 tiles: gs = 6 on all 148 SMs instead of
-    // 8 on 98 SMs; c5: 6; c3: 8)
+    // tiles per row group: the CTAs share the (row group, subspace) pairs in contiguous ranges, so
+    // the largest row group (kG tiles: the most codebook-image reuse) balances to within a pair
     int gs = kG;
-    double busiest = -1.0;
-    for (int g = kG; g >= 1; --g) {
-        const double cost = (double)(((ntiles + g - 1) / g + sms - 1) / sms * g) * (1.0 + 0.5 / g);
-        if (busiest < 0.0 || cost < busiest) { busiest = cost; gs = g; }
-    }
     if (const char *ge = getenv("CSPQ_TC_GS")) gs = std::max(1, std::min(kG, atoi(ge)));  // debug override
     const int64_t ngroups = (ntiles + gs - 1) / gs;
-    const int grid = (int)std::min<int64_t>(sms, ngroups);
+    CSPQ_REQUIRE(ngroups * m < ((int64_t)1 << 31), CSPQ_E_CONFIG, "too many rows (%lld) for one launch", (long long)n);
+    const int grid = (int)std::min<int64_t>(sms, ngroups * m);
     kern<<<grid, kThreads, smem, st>>>(X, n, m, xs, xjs, CB, B, guard, img, codes, cs, cjs, flags, best, gs, probe);
     CSPQ_LAUNCH_CHECK();
     return CSPQ_OK;
