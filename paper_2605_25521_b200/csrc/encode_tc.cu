@@ -44,6 +44,7 @@
 //               item (x prefetched with cp.async, tf32 split), selects the winner and
 //               runner-up, applies the error-band guard and the exact fix-up, stores codes.
 
+#include <atomic>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -674,15 +675,31 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const flo
 #endif
     auto kern = flags ? (best ? encode_tc_kernel<SUB, TIn, true, true> : encode_tc_kernel<SUB, TIn, true, false>)
                       : (best ? encode_tc_kernel<SUB, TIn, false, true> : encode_tc_kernel<SUB, TIn, false, false>);
-    CSPQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, sms = 148;
+    // per-launch host work kept to the launch itself (small batches -- c5's 4096 rows -- launch
+    // often): the shared-memory opt-in is set once per (device, kernel) at the maximum, the SM
+    // count read once per device
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static int sm_count[64] = {};
+    static std::atomic<uint32_t> smem_set[64][2][2] = {};  // [device][mark][best] (statics are per SUB, TIn)
+    const int di = dev & 63;
+    if (!sm_count[di]) {
+        int v = 148;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        sm_count[di] = v;
+    }
+    const int sms = sm_count[di];
+    std::atomic<uint32_t> &once = smem_set[di][flags ? 1 : 0][best ? 1 : 0];
+    if (!once.load(std::memory_order_acquire)) {
+        CSPQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        once.store(1, std::memory_order_release);
+    }
     const int64_t ntiles = (n + kTM - 1) / kTM;
     // tiles per row group: the CTAs share the (row group, subspace) pairs in contiguous ranges, so
     // the largest row group (kG tiles: the most codebook-image reuse) balances to within a pair
     int gs = kG;
-    if (const char *ge = getenv("CSPQ_TC_GS")) gs = std::max(1, std::min(kG, atoi(ge)));  // debug override
+    static const int gs_env = [] { const char *ge = getenv("CSPQ_TC_GS"); return ge ? atoi(ge) : 0; }();
+    if (gs_env) gs = std::max(1, std::min(kG, gs_env));  // debug override
     const int64_t ngroups = (ntiles + gs - 1) / gs;
     CSPQ_REQUIRE(ngroups * m < ((int64_t)1 << 31), CSPQ_E_CONFIG, "too many rows (%lld) for one launch", (long long)n);
     const int grid = (int)std::min<int64_t>(sms, ngroups * m);
