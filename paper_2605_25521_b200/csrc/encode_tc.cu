@@ -35,14 +35,16 @@
 //   with sum|x_t c_t| <= ||x|| max_l ||c_l||; a runner-up within 4E (x2
 //   safety) of the best is flagged.
 //
-// Warp roles (64 + 128 kGroups threads, one CTA per SM, persistent over row groups):
-//   warp 0      TMEM allocation + MMA issue (one lane)
+// Warp roles (64 + 128 kGroups threads, one CTA per SM, persistent over a contiguous range of
+// (row group, subspace) pairs):
+//   warp 0      TMEM allocation + MMA issue (the warp walks the items, one elected lane issues)
 //   warp 1      bulk copies of the prepared codebook image + fp32 codebook (cp.async.bulk)
 //   warps 2..   kGroups epilogue groups of 4 warps (TMEM lane quadrant = warp % 4); item it
 //               belongs to group it % kGroups and TMEM buffer it & 1.  A group drains its
 //               item's accumulator (block + class minima), writes the A operand of its next
-//               item (x prefetched with cp.async, tf32 split), selects the winner and
-//               runner-up, applies the error-band guard and the exact fix-up, stores codes.
+//               item (x prefetched with cp.async, tf32 split), selects the winner with the
+//               band indicators (runner-up within the error band => flag), applies the exact
+//               fix-up (or, in mark mode, flags the pair for the caller), stores codes.
 
 #include <atomic>
 #include <cstdlib>
@@ -236,8 +238,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                  float *__restrict__ best_out, int gs, int probe) {
     // probe (debug timing only; honoured by -DCSPQ_TC_PROBES builds): bit 0 = epilogue skips its min work, bit 1 = no MMAs,
     // bit 2 = skip the A conversion, bit 3 = keep TMEM loads but skip the min work
-    // (bits 0-3 leave garbage codes), bit 4 = CTA 0 writes clock64 stamps into best_out,
-    // bit 5 = no x prefetch (stale x), bit 6 = no code stores
+    // (bits 0-3 leave garbage codes), bit 4 = CTA 0 writes clock64 stamps into best_out
+    // (-DCSPQ_TC_STAMPS), bit 5 = no x prefetch (stale x), bit 6 = no code stores, bit 7 = no
+    // selection / fix-up
     using S = TcShape<SUB>;
     using L = TcSmem<SUB, TIn>;
 #ifdef CSPQ_TC_STAMPS
