@@ -125,6 +125,9 @@ int cspq_encode_with_scores(const void *X, int32_t in_dtype, int64_t n, int32_t 
  * best (optional, (n, m) float32) receives the tensor-core score of each
  * winner (diagnostics). */
 size_t cspq_encode_tc_image_bytes(int32_t m, int32_t k, int32_t sub);
+/* Largest m the tensor-core kernel takes for this sub / in_dtype (0: sub unsupported); callers
+ * use cspq_encode beyond it. */
+int32_t cspq_encode_tc_max_subspaces(int32_t sub, int32_t in_dtype);
 int cspq_encode_tc_prepare(const float *CB, const float *B, int32_t m, int32_t k, int32_t sub, void *img,
                            void *stream);
 int cspq_encode_tc(const void *X, int32_t in_dtype, int64_t n, int32_t d, int64_t x_row_stride,

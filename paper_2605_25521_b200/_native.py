@@ -38,6 +38,7 @@ _SIGS = {
     "cspq_encode_stats": ([_vp, _i32], _i32),
     "cspq_encode_set_tiling": ([_i32], _i32),
     "cspq_encode_tc_image_bytes": ([_i32, _i32, _i32], ctypes.c_size_t),
+    "cspq_encode_tc_max_subspaces": ([_i32, _i32], _i32),
     "cspq_encode_tc_prepare": ([_vp, _vp, _i32, _i32, _i32, _vp, _vp], _i32),
     "cspq_encode_tc": ([_vp, _i32, _i64, _i32, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _i64, _vp, _vp], _i32),
     "cspq_encode_prepare": ([_vp, _vp, _i32, _i32, _i32, _vp, _vp], _i32),

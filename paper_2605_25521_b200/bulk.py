@@ -192,9 +192,15 @@ def _variant_args(cbset: CodebookSet, plan: ExecutionPlan, precomputed_bias: boo
     return rm, bs, guard, vid
 
 
+def _tc_shape_ok(cbset, in_u8: bool) -> bool:
+    """k = 256, sub in {4, 8} and not more subspaces than the tensor-core kernel's shared memory holds."""
+    return (cbset.k == 256 and cbset.sub_dim in (4, 8)
+            and cbset.m <= N.load().cspq_encode_tc_max_subspaces(cbset.sub_dim, N.IN_U8 if in_u8 else N.IN_F32))
+
+
 def _tc_ok(X, xrs, cbset) -> bool:
     t = torch()
-    if cbset.k != 256 or cbset.sub_dim not in (4, 8):
+    if not _tc_shape_ok(cbset, X.dtype == t.uint8):
         return False
     if X.dtype == t.uint8:
         return True
@@ -237,8 +243,8 @@ def encode_dataset_device(X, codebooks, plan: ExecutionPlan | None = None, *,
     mode = plan.mode
     use_tc = mode in ("auto", "tensor") and vid != N.VARIANT_REFERENCE and _tc_ok(X, xrs, cbset)
     if mode == "tensor" and not use_tc:
-        raise ConfigError("mode='tensor' needs k=256, sub_dim in {4, 8}, a REFORMULATED/BLOCKED variant "
-                          "and 16-byte aligned rows")
+        raise ConfigError("mode='tensor' needs k=256, sub_dim in {4, 8}, a REFORMULATED/BLOCKED variant, "
+                          "16-byte aligned rows and at most cspq_encode_tc_max_subspaces subspaces")
     if best is not None and not use_tc:
         raise ConfigError("best (winning tensor-core scores) is only produced by the tensor-core path")
     with t.cuda.device(dev):
@@ -310,10 +316,11 @@ def encode_dataset_host(X: np.ndarray, codebooks, plan: ExecutionPlan | None = N
     if batch_ms is not None and batch_ms.shape[0] < nb:
         raise ConfigError("batch_ms too small")
     img = None
-    if plan.mode in ("auto", "tensor") and vid != N.VARIANT_REFERENCE and cbset.k == 256 and cbset.sub_dim in (4, 8):
+    if plan.mode in ("auto", "tensor") and vid != N.VARIANT_REFERENCE and _tc_shape_ok(cbset, in_u8):
         img = cbset.tc_image(dev, nobias=not precomputed_bias and plan.variant is EncoderVariant.BLOCKED)
     elif plan.mode == "tensor":
-        raise ConfigError("mode='tensor' needs k=256, sub_dim in {4, 8} and a REFORMULATED/BLOCKED variant")
+        raise ConfigError("mode='tensor' needs k=256, sub_dim in {4, 8}, a REFORMULATED/BLOCKED variant and "
+                          "at most cspq_encode_tc_max_subspaces subspaces")
     t.cuda.current_stream(dev).synchronize()  # image preparation visible to the pipeline streams
     N.call("cspq_encode_host", X.ctypes.data_as(ctypes.c_void_p), N.IN_U8 if in_u8 else N.IN_F32, n, d,
            ptr(rm), ptr(bs), ptr(guard), ptr(img), cbset.m, cbset.k, cbset.sub_dim,

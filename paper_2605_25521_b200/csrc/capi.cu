@@ -23,6 +23,7 @@ int encode_tc(const void *X, int in_dtype, int64_t n, int64_t xrs, const float *
               const float *guard, const void *img, int m, int k, int sub, uint8_t *codes, int64_t crs, float *best,
               cudaStream_t st);
 int encode_tc_stats(unsigned long long *flagged, int reset);
+int encode_tc_max_subspaces(int sub, int in_dtype);
 int recompute_biases(const float *CB, int m, int k, int sub, float *Bo, cudaStream_t st);
 int encode_device(const void *X, int in_dtype, int64_t n, int d, int64_t xrs, const float *CB, const float *B,
                   const float *guard, int m, int k, int sub, void *codes, int64_t crs, int variant, int mode,
@@ -203,6 +204,8 @@ int cspq_encode_tc(const void *X, int32_t in_dtype, int64_t n, int32_t d, int64_
     return encode_tc(X, in_dtype, n, x_row_stride, CB, B, guard, img, m, k, sub, reinterpret_cast<uint8_t *>(codes),
                      codes_row_stride, best, as_stream(stream));
 }
+
+int32_t cspq_encode_tc_max_subspaces(int32_t sub, int32_t in_dtype) { return encode_tc_max_subspaces(sub, in_dtype); }
 
 int cspq_encode_prepare(const float *CB, const float *B, int32_t m, int32_t k, int32_t sub, float *guard,
                         void *stream) {

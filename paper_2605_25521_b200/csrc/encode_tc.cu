@@ -755,6 +755,14 @@ int encode_tc(const void *X, int in_dtype, int64_t n, int64_t xrs, const float *
     return encode_tc_ex(X, in_dtype, n, xrs, sub, CB, B, guard, img, m, k, sub, codes, crs, 1, nullptr, best, st);
 }
 
+// the largest m whose guard constants fit next to the kernel's fixed shared-memory layout
+int encode_tc_max_subspaces(int sub, int in_dtype) {
+    auto fit = [](size_t fixed) { return (int)((227 * 1024 - fixed - sizeof(TcSmemHdr) - 16) / 8 / 4 * 4); };
+    if (sub == 8) return in_dtype == CSPQ_IN_U8 ? fit(TcSmem<8, uint8_t>::oG) : fit(TcSmem<8, float>::oG);
+    if (sub == 4) return in_dtype == CSPQ_IN_U8 ? fit(TcSmem<4, uint8_t>::oG) : fit(TcSmem<4, float>::oG);
+    return 0;
+}
+
 int encode_tc_stats(unsigned long long *flagged, int reset) {
     if (flagged) CSPQ_CUDA_TRY(cudaMemcpyFromSymbol(flagged, g_tc_flagged, sizeof(unsigned long long)));
     if (reset) {

@@ -930,6 +930,7 @@ size_t lloyd_workspace_bytes(int64_t n, int m, int sub, int k) { return (size_t)
 
 int encode_prepare(const float *CB, const float *B, int m, int k, int sub, float *guard, cudaStream_t st);
 int encode_tc_prepare(const float *CB, const float *B, int m, int k, int sub, void *img, cudaStream_t st);
+int encode_tc_max_subspaces(int sub, int in_dtype);
 int encode_tc_ex(const void *X, int in_dtype, int64_t n, int64_t xrs, int64_t xjs, const float *CB, const float *B,
                  const float *guard, const void *img, int m, int k, int sub, uint8_t *codes, int64_t crs, int64_t cjs,
                  uint8_t *flags, float *best, cudaStream_t st);
@@ -970,7 +971,8 @@ int lloyd_assign(const void *P, int pf64, int64_t n, int m, int sub, int k, cons
     if (e <= b) return CSPQ_OK;
     const char *tcv = getenv("CSPQ_LLOYD_TC");  // "0": the plain float64 kernel (A/B and tests)
     const bool tc_on = !(tcv && tcv[0] == '0');
-    if (tc_on && !pf64 && k == 256 && (sub == 4 || sub == 8) && reinterpret_cast<uintptr_t>(P) % 16 == 0)
+    if (tc_on && !pf64 && k == 256 && (sub == 4 || sub == 8) && reinterpret_cast<uintptr_t>(P) % 16 == 0 &&
+        m <= encode_tc_max_subspaces(sub, CSPQ_IN_F32))
         return assign_tc(reinterpret_cast<const float *>(P), n, m, sub, k, C64, cn, state, b, e, assign, sq, ws, L, st);
     const size_t need = (size_t)k * (sub + 1) * sizeof(double);
     const int use_smem = need <= 96 * 1024;

@@ -154,3 +154,27 @@ def test_large_common_offset_tensor(P, oracle, offset):
     want = oracle.encode(X, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM)
     got = tc_codes(P, X, cs)
     assert got.tobytes() == want.tobytes(), int((got != want).sum())
+
+
+def test_too_many_subspaces_for_tensor_kernel(P, oracle):
+    """Beyond cspq_encode_tc_max_subspaces (the kernel's guard constants live in shared memory),
+    'auto' falls back to the FFMA kernel (same codes) and 'tensor' refuses; Lloyd's screened
+    assignment falls back to the float64 kernel."""
+    from paper_2605_25521_b200 import _native as N
+    import torch
+    m = N.load().cspq_encode_tc_max_subspaces(8, N.IN_F32) + 4
+    rng = np.random.default_rng(3)
+    n, sub = 200, 8
+    rm = rng.standard_normal((m, 256, sub)).astype(np.float32)
+    X = rng.standard_normal((n, m * sub)).astype(np.float32)
+    cs = cset_of(P, rm)
+    want = oracle.encode(X, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM)
+    Xd = torch.from_numpy(X).cuda()
+    assert P.encode_dataset_device(Xd, cs, P.ExecutionPlan(mode="auto")).cpu().numpy().tobytes() == want.tobytes()
+    assert P.encode_dataset(X, cs).codes.tobytes() == want.tobytes()
+    with pytest.raises(P.ConfigError, match="tensor"):
+        P.encode_dataset_device(Xd, cs, P.ExecutionPlan(mode="tensor"))
+    pts = np.ascontiguousarray(X[:, :].reshape(n, m, sub).transpose(1, 0, 2)[:, :, :])
+    init = np.ascontiguousarray(np.repeat(pts[:, :1], 256, axis=1).astype(np.float64) + rm.astype(np.float64))
+    res = P.lloyd_iterate_batched(pts, init, P.TrainConfig(k=256, max_iters=2, tol=0.0))
+    assert len(res) == m and all(r.iterations >= 1 for r in res)

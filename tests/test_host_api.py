@@ -178,3 +178,11 @@ def test_execution_plan_devices_validation():
     for bad in ([], [-1], [0.5], ["0"]):
         with pytest.raises(P.ConfigError, match="devices"):
             P.ExecutionPlan(devices=bad)
+
+
+def test_tensor_kernel_subspace_limit_query():
+    L = N.load()
+    for sub in (4, 8):
+        for dt in (N.IN_F32, N.IN_U8):
+            assert L.cspq_encode_tc_max_subspaces(sub, dt) >= 256  # every configuration (m <= 192) fits
+    assert L.cspq_encode_tc_max_subspaces(16, N.IN_F32) == 0
