@@ -65,7 +65,9 @@ def workload_desc(cfg, rows_per_rank, ws, scaling):
     return (f"{cfg.name}: {'u8' if cfg.dtype == 'u8' else 'f32'} rows D={cfg.d}, M={cfg.m} (d_sub={cfg.sub}), "
             f"K={cfg.k}, {rows_per_rank:,} rows/GPU ({scaling} scaling), codebooks: "
             + (f"{cfg.iters} Lloyd iters on a {cfg.n_train:,}-row sample" if cfg.codebook == "lloyd"
-               else "256 distinct data subvectors per subspace"))
+               else "256 distinct data subvectors per subspace")
+            + ("; timed steps encode, the training is timed once in train.* (train_plus_encode_vec_s: both)"
+               if cfg.name == "c2" else ""))
 
 
 def oracle_codebooks(cfg, dev):
