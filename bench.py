@@ -348,6 +348,17 @@ def main():
             "note": f"the MMA executes K={k_eff} tf32 per (row, subspace) for {cfg.sub} useful MACs "
                     "(hi/lo split + folded bias); the epilogue's min/max on the half-rate ALU pipe is the binding unit",
         }
+        # the binding unit: an exact argmin with an exact runner-up over K scores needs two min
+        # trees (block and class minima) -- K three-input min lane-operations per (row, subspace) --
+        # on the ALU pipe (16 lanes / clk / SMSP, scripts/micro/mnmx_peak.cu)
+        alu_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 4 * 16 * 1.965e9
+        alu_ops = rows * cfg.m * cfg.k / (ms_per_step / 1e3)
+        roofline["alu"] = {
+            "algorithmic_min_lane_ops_per_row": cfg.m * cfg.k, "achieved_lane_ops_per_s": alu_ops,
+            "peak_lane_ops_per_s": alu_peak, "frac": alu_ops / alu_peak,
+            "note": "FMNMX3 lane-ops of the two min trees only; ncu shows the ALU pipe ~56 % busy in total "
+                    "(the rest: predicates, loop and address arithmetic), profiles/r1_ncu_full_encode_c3_tc.json",
+        }
     # ---- c2's timed scope is train + encode: report the GPU Lloyd beside the encode ----
     train = None
     if rank == 0 and cfg.codebook == "lloyd" and cfg.name == "c2":
