@@ -1,3 +1,5 @@
+"""Flag rate of the tensor-core screen inside the Lloyd training (c2/c3/c4 samples): the share of
+(point, subspace) pairs that take the float64 settle scan."""
 import sys, os, ctypes
 sys.path.insert(0, os.getcwd())
 import torch, paper_2605_25521_b200 as P

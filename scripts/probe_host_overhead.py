@@ -1,3 +1,4 @@
+"""Host-side cost per encode call: the Python API (encode_dataset_device) and the raw C call."""
 import sys, os, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch

@@ -1,3 +1,4 @@
+"""Time the batched GPU k-means++ seeding."""
 import sys, os, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch

@@ -1,4 +1,5 @@
-# needs a -DCSPQ_TC_PROBES -DCSPQ_TC_STAMPS build (scripts/ab_build.sh, CSPQ_LIB_PATH)
+"""clock64 stamps of the tensor-core kernel's roles per item (CTA 0): MMA waits / issue, scan
+ phases, epilogue.  Needs a -DCSPQ_TC_PROBES -DCSPQ_TC_STAMPS build (scripts/ab_build.sh, CSPQ_LIB_PATH)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["CSPQ_TC_PROBE"] = sys.argv[1] if len(sys.argv) > 1 else "16"
