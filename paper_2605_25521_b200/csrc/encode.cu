@@ -330,9 +330,22 @@ encode_generic_kernel(const TIn *__restrict__ X, int64_t n, int m, int k, int su
     const int sub = SUBC > 0 ? SUBC : sub_rt;
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y;
+    const float *C = CB + (int64_t)j * k * sub;
+    // REFERENCE: cc_l = sum_t c_t * c_t does not depend on the row -- the CTA computes the
+    // subspace's chains once (the same ascending mul-then-add, so the same bits) for k <= 1024
+    constexpr int kCcMax = 1024;
+    __shared__ float s_cc[VARIANT == CSPQ_VARIANT_REFERENCE ? kCcMax : 1];
+    const bool cc_tab = VARIANT == CSPQ_VARIANT_REFERENCE && k <= kCcMax;
+    if (cc_tab) {
+        for (int l = threadIdx.x; l < k; l += blockDim.x) {
+            float cc = 0.f;
+            for (int t = 0; t < sub; ++t) { const float cv = __ldg(C + (int64_t)l * sub + t); cc = __fadd_rn(cc, __fmul_rn(cv, cv)); }
+            s_cc[l] = cc;
+        }
+        __syncthreads();
+    }
     if (row >= n) return;
     const TIn *x = X + row * xrs + (int64_t)j * xss;
-    const float *C = CB + (int64_t)j * k * sub;
     float best = pos_inf_f();
     int bidx = 0;
     if constexpr (SUBC > 0) {
@@ -349,11 +362,17 @@ encode_generic_kernel(const TIn *__restrict__ X, int64_t n, int m, int k, int su
             float s;
             if constexpr (VARIANT == CSPQ_VARIANT_REFERENCE) {
                 float cc = 0.f, dd = 0.f;
+                if (cc_tab) {
+                    cc = s_cc[l];
 #pragma unroll
-                for (int t = 0; t < SUBC; ++t) {
-                    const float cv = __ldg(c + t);
-                    cc = __fadd_rn(cc, __fmul_rn(cv, cv));
-                    dd = __fadd_rn(dd, __fmul_rn(xv[t], cv));
+                    for (int t = 0; t < SUBC; ++t) dd = __fadd_rn(dd, __fmul_rn(xv[t], __ldg(c + t)));
+                } else {
+#pragma unroll
+                    for (int t = 0; t < SUBC; ++t) {
+                        const float cv = __ldg(c + t);
+                        cc = __fadd_rn(cc, __fmul_rn(cv, cv));
+                        dd = __fadd_rn(dd, __fmul_rn(xv[t], cv));
+                    }
                 }
                 s = __fsub_rn(__fadd_rn(vv, cc), __fmul_rn(2.0f, dd));
             } else {
@@ -377,9 +396,10 @@ encode_generic_kernel(const TIn *__restrict__ X, int64_t n, int m, int k, int su
                 for (int t = 0; t < sub; ++t) {
                     const float v = to_f(x[t]);
                     const float cv = __ldg(c + t);
-                    cc = __fadd_rn(cc, __fmul_rn(cv, cv));
+                    if (!cc_tab) cc = __fadd_rn(cc, __fmul_rn(cv, cv));
                     dd = __fadd_rn(dd, __fmul_rn(v, cv));
                 }
+                if (cc_tab) cc = s_cc[l];
                 s = __fsub_rn(__fadd_rn(vv, cc), __fmul_rn(2.0f, dd));
             } else {
                 float dd = 0.f;
