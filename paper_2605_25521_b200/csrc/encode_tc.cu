@@ -254,7 +254,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
     // across chunks and spills at the 128-register cap
     probe &= 8;
 #endif
-    if (probe & 16) best_out = nullptr;
+#ifdef CSPQ_TC_STAMPS
+    if (probe & 16) best_out = nullptr;  // (the stamps borrow best_out)
+#endif
     constexpr int kStampItems = 2048;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sB = smem_raw + L::oB;

@@ -387,7 +387,7 @@ assign_kernel(const TP *__restrict__ P, int64_t n, int k, int sub_rt, const doub
             }
         }
         return;
-    }
+    } else {
     for (int64_t i = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
         double best = 0.0;
         int bi = 0;
@@ -406,6 +406,7 @@ assign_kernel(const TP *__restrict__ P, int64_t n, int k, int sub_rt, const doub
         const double v = __dadd_rn(best, xx);
         assign[(int64_t)j * n + i] = bi;
         sq[(int64_t)j * n + i] = (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(v, 0.0)
+    }
     }
 }
 
