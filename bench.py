@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--e2e-rows", type=int, default=0,
                    help="rows per rank through the host API (0 = max(2M, 6 GB of rows), or the whole config for c5)")
     p.add_argument("--streams", type=int, default=0, help="host pipeline streams (0 = 3, or 6 for c5)")
-    p.add_argument("--e2e-batch", type=int, default=0, help="host pipeline batch rows (0 = max(131072, 256 MB of rows), or 4096 for c5)")
+    p.add_argument("--e2e-batch", type=int, default=0, help="host pipeline batch rows (0 = max(131072 rows, 256 MB) capped at a quarter of the sample, or 4096 for c5)")
     p.add_argument("--train", choices=["auto", "sharded", "rank0"], default="auto",
                    help="codebook training: row-sharded Lloyd with one all-reduce per iteration (auto: when N > 1), "
                         "or the fused single-GPU cspq_lloyd_train on rank 0 + broadcast")
@@ -276,6 +276,9 @@ def main():
         row_bytes = cfg.d * cfg.elem_bytes
         ne = min(args.e2e_rows or (cfg.n if cfg.batch else max(2_000_000, (6 << 30) // row_bytes)), rows)
         batch_rows = cfg.batch or args.e2e_batch or max(1 << 17, (256 << 20) // row_bytes)
+        if not (cfg.batch or args.e2e_batch):
+            # at least 4 batches so encode and D2H overlap the next H2D (c1's 100K rows: 4 x 25K)
+            batch_rows = min(batch_rows, max(1 << 14, -(-ne // 4)))
         Xh = P.pinned_empty((ne, cfg.d), np.uint8 if cfg.dtype == "u8" else np.float32)
         Xh[:] = X[:ne].cpu().numpy()
         codes_h = P.pinned_empty((ne, cfg.m), np.uint8)
@@ -302,7 +305,7 @@ def main():
                "streams": eplan.streams,
                "batch_latency_ms": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
                                     "batches": int(lat.shape[0]),
-                                    "def": "device events: H2D start -> D2H end of one batch (3 batches in flight)"},
+                                    "def": f"device events: H2D start -> D2H end of one batch ({eplan.streams} batches in flight)"},
                "h2d_GBps": ne * cfg.d * cfg.elem_bytes * args.steps / float(el.item()) / 1e9,
                "path": "encode_dataset_host (pinned numpy -> cspq_encode_host: multi-stream H2D/encode/D2H pipeline)"}
 
