@@ -65,7 +65,8 @@ constexpr int kNA = kGroups; // A-operand stages (a group writes item it + kGrou
 constexpr int kThreads = 64 + 128 * kGroups;  // MMA warp, loader warp, kGroups x 4 epilogue warps
 constexpr int kNC = 1;        // accumulator chunks per item (N = 256 / kNC per MMA, own commit + barriers):
                               // MMA and scan overlap chunk by chunk; measured on c3: 1 = 2.16e8 vec/s,
-                              // 2 = 2.04e8, 4 = 1.44e8 (an N=64 MMA costs almost what an N=256 one does)
+                              // 2 = 2.04e8, 4 = 1.44e8 (an N=64 MMA costs almost what an N=256 one does);
+                              // re-measured on the final kernel: 1 = 2.73e8 / c4 8.68e8, 2 = 2.61e8 / 8.35e8
 constexpr int kCW = 256 / kNC;  // chunk width in TMEM columns (a multiple of 64: one tcgen05.ld x64)
 constexpr int kPD = 2;        // cp.async prefetch distance, in the group's own items
 constexpr int kRing = 3;      // x slots per group (> kPD: an item's slot outlives its fix-up)
