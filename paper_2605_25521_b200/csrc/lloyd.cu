@@ -456,17 +456,22 @@ tc_settle_kernel(const float *__restrict__ P, int64_t n, int k, const double *__
         for (int t = 0; t < SUBC; ++t) dot = __fma_rn(x[t], c[t], dot);
         return __fma_rn(-2.0, dot, cnj[l]);
     };
-    // two points per thread per step (independent loads in flight); x with 16-byte loads
+    // two points per thread per step (independent loads in flight); x with 16-byte loads.  The
+    // loop bound is warp-uniform (a warp owns 64 consecutive points) so flagged points can be
+    // scanned by the whole warp: lanes split the 256 centroids, then a shuffle reduction keeps the
+    // sequential scan's winner (smallest d, first index; a NaN d never wins unless it is d_0)
     constexpr int kPP = 2;
+    const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kPP;
-    for (int64_t i0 = b + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kPP; i0 < e; i0 += stride) {
+    for (int64_t w0 = b + ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * kPP; w0 < e; w0 += stride) {
+        const int64_t i0 = w0 + lane * kPP;
         double x[kPP][SUBC];
         int bi[kPP];
         bool fl[kPP], ok[kPP];
 #pragma unroll
         for (int p = 0; p < kPP; ++p) {
             ok[p] = i0 + p < e;
-            const int64_t ji = (int64_t)j * n + (ok[p] ? i0 + p : i0);
+            const int64_t ji = (int64_t)j * n + (ok[p] ? i0 + p : b);
             const float4 *xp = reinterpret_cast<const float4 *>(P + ji * SUBC);
 #pragma unroll
             for (int q = 0; q < SUBC / 4; ++q) {
@@ -474,29 +479,53 @@ tc_settle_kernel(const float *__restrict__ P, int64_t n, int k, const double *__
                 x[p][4 * q] = v.x; x[p][4 * q + 1] = v.y; x[p][4 * q + 2] = v.z; x[p][4 * q + 3] = v.w;
             }
             bi[p] = codes[ji];
-            fl[p] = flags[ji] != 0;
+            fl[p] = ok[p] && flags[ji] != 0;
         }
-#pragma unroll
-        for (int p = 0; p < kPP; ++p) {
-            if (!ok[p]) break;
-            const int64_t ji = (int64_t)j * n + i0 + p;
-            double best;
-            if (fl[p]) {  // full float64 scan, first index on ties (assign_kernel's order)
-                best = 0.0;
-                bi[p] = 0;
-                for (int l = 0; l < k; ++l) {
-                    const double d1 = dist(x[p], l);
-                    if (l == 0 || d1 < best) { best = d1; bi[p] = l; }
-                }
-            } else {
-                best = dist(x[p], bi[p]);
-            }
+        auto finish = [&](const double (&xv)[SUBC], int64_t ji, int l, double d) {
             double xx = 0.0;
 #pragma unroll
-            for (int t = 0; t < SUBC; ++t) xx = __dadd_rn(xx, __dmul_rn(x[p][t], x[p][t]));
-            const double v = __dadd_rn(best, xx);
-            assign[ji] = bi[p];
+            for (int t = 0; t < SUBC; ++t) xx = __dadd_rn(xx, __dmul_rn(xv[t], xv[t]));
+            const double v = __dadd_rn(d, xx);
+            assign[ji] = l;
             sq[ji] = (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(v, 0.0)
+        };
+#pragma unroll
+        for (int p = 0; p < kPP; ++p)
+            if (ok[p] && !fl[p]) finish(x[p], (int64_t)j * n + i0 + p, bi[p], dist(x[p], bi[p]));
+#pragma unroll
+        for (int p = 0; p < kPP; ++p) {
+            unsigned todo = __ballot_sync(0xffffffffu, fl[p]);
+            while (todo) {  // full float64 scan of one flagged point by the whole warp
+                const int src = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const int64_t ji = (int64_t)j * n + w0 + src * kPP + p;
+                double xs[SUBC];
+                const float4 *xp = reinterpret_cast<const float4 *>(P + ji * SUBC);
+#pragma unroll
+                for (int q = 0; q < SUBC / 4; ++q) {
+                    const float4 v = xp[q];
+                    xs[4 * q] = v.x; xs[4 * q + 1] = v.y; xs[4 * q + 2] = v.z; xs[4 * q + 3] = v.w;
+                }
+                double bd = 0.0;
+                int bl = -1;
+#pragma unroll 1
+                for (int r = 0; r < 8; ++r) {  // k == 256: centroids lane + 32 r, ascending
+                    const int l = lane + 32 * r;
+                    const double d1 = dist(xs, l);
+                    if (d1 == d1 && (bl < 0 || d1 < bd)) { bd = d1; bl = l; }
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                    const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                    if (ol >= 0 && (bl < 0 || od < bd || (od == bd && ol < bl))) { bd = od; bl = ol; }
+                }
+                if (lane == 0) {
+                    const double d0 = dist(xs, 0);
+                    if (d0 != d0 || bl < 0) { bl = 0; bd = d0; }  // d_0 NaN (or every d NaN): index 0 stays
+                    finish(xs, ji, bl, bd);
+                }
+            }
         }
     }
 }
