@@ -73,6 +73,13 @@ constexpr int kRing = 3;      // x slots per group (> kPD: an item's slot outliv
 constexpr int kScrW = 36;     // floats per row of the block-minima scratch: 32 + 4 pad, so the 16-B
                               // stores / loads of 8 consecutive rows hit 8 distinct bank quads
 
+// error constant E of the tensor scores: |S - s_oracle| <= E W, W = max|b| + ||x|| max||c||
+// (tf32 split, 2 roundings per K = 8 step, the oracle's own chain; 1 % slack).  Lloyd's final
+// REFERENCE screen widens the same band (lloyd.cu, final_guard_kernel)
+__host__ __device__ constexpr float tc_error_constant(int sub) {
+    return (float)((4.0 / 4194304.0 + (sub == 8 ? 4 : 2) / 4194304.0 * (1.0 + 1.0 / 1024.0) + (sub + 1) / 16777216.0) * 1.01);
+}
+
 template <int SUB>
 struct TcShape {
     static constexpr int K = SUB == 8 ? 32 : 16;    // tf32 elements per operand row
@@ -368,7 +375,8 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         const int q = warp & 3;
         const int r = 32 * q + lane;
         float *scratch = sScr + ((size_t)e * kTM + r) * kScrW;  // this thread's 32 block minima
-        constexpr float kE = (float)((4.0 / 4194304.0 + S::kSteps / 4194304.0 * (1.0 + 1.0 / 1024.0) + (SUB + 1) / 16777216.0) * 1.01);
+        constexpr float kE = tc_error_constant(SUB);
+        static_assert(S::kSteps == (SUB == 8 ? 4 : 2), "tc_error_constant counts K = 8 MMA steps");
         // the group's x ring: owned item k (item e + kGroups k) lives in slot k % kRing
         static_assert(kRing == kPD + 1, "slot rotation below assumes kRing == kPD + 1");
         auto ring = [&](int slot) -> unsigned char * {
@@ -759,6 +767,8 @@ int encode_tc(const void *X, int in_dtype, int64_t n, int64_t xrs, const float *
 }
 
 // the largest m whose guard constants fit next to the kernel's fixed shared-memory layout
+float encode_tc_error_constant(int sub) { return tc_error_constant(sub); }
+
 int encode_tc_max_subspaces(int sub, int in_dtype) {
     auto fit = [](size_t fixed) { return (int)((227 * 1024 - fixed - sizeof(TcSmemHdr) - 16) / 8 / 4 * 4); };
     if (sub == 8) return in_dtype == CSPQ_IN_U8 ? fit(TcSmem<8, uint8_t>::oG) : fit(TcSmem<8, float>::oG);

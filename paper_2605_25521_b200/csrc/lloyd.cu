@@ -47,7 +47,7 @@ struct WsLayout {
     // float32 copy of float64 points (final pass), k-means++ scratch
     int64_t p32, d2, pp;
     // tensor-core screened assignment: float32 codebooks, biases, guard, tcgen05 image, codes, flags
-    int64_t tc_cb, tc_b, tc_guard, tc_img, tc_codes, tc_flags;
+    int64_t tc_cb, tc_b, tc_guard, tc_img, tc_codes, tc_flags, tc_rmax;
     int64_t total;
     int64_t nch, maxleaves;
     WsLayout(int64_t n, int m, int sub, int k) {
@@ -85,6 +85,7 @@ struct WsLayout {
         tc_img = take((int64_t)m * k * 32 * 4);  // K = 32 tf32 per centroid row at most
         tc_codes = take((int64_t)m * n);
         tc_flags = take((int64_t)m * n);
+        tc_rmax = take(4 * (int64_t)m);
         total = o;
     }
     template <typename T>
@@ -961,6 +962,7 @@ size_t lloyd_workspace_bytes(int64_t n, int m, int sub, int k) { return (size_t)
 int encode_prepare(const float *CB, const float *B, int m, int k, int sub, float *guard, cudaStream_t st);
 int encode_tc_prepare(const float *CB, const float *B, int m, int k, int sub, void *img, cudaStream_t st);
 int encode_tc_max_subspaces(int sub, int in_dtype);
+float encode_tc_error_constant(int sub);
 int encode_tc_ex(const void *X, int in_dtype, int64_t n, int64_t xrs, int64_t xjs, const float *CB, const float *B,
                  const float *guard, const void *img, int m, int k, int sub, uint8_t *codes, int64_t crs, int64_t cjs,
                  uint8_t *flags, float *best, cudaStream_t st);
@@ -991,6 +993,141 @@ static int assign_tc(const float *P, int64_t n, int m, int sub, int k, const dou
     return CSPQ_OK;
 }
 
+// ---------------------------------------------------------------- screened final pass
+// The final assignment is the float32 REFERENCE encoder (training.py:143-150, kernels.py:84-105):
+// dist_l = (vv + cc_l) - 2 dd_l with every product and sum rounded in sequence, strict < from
+// +inf.  Each term is a d_sub-long recursive sum, so |dist_l - D_l| <= g (vv + cc_l + 2 |x| |c_l|)
+// with g = gamma_{d_sub + 4} for the real D_l = |x|^2 + 2 s_l (s_l = |c_l|^2 / 2 - x.c_l).  The
+// tensor kernel screens s_l; its band is widened from E W to E W + u max|b| + g (max|b| +
+// |x| max|c| + |x| R / 2) (R = max |x| of the subspace's points, so vv / 2 <= |x| R / 2; u
+// covers the rounding of b).  An unflagged point's winner then beats every other centroid's
+// REFERENCE distance by > 7.8 E'W' - 4 (E'W') > 0: its code is the REFERENCE code.  Flagged
+// points take the exact REFERENCE scan, the whole warp on one point.
+__global__ void pnorm_max_kernel(const float *__restrict__ P, int64_t n, int sub, unsigned *__restrict__ rmax) {
+    const int j = blockIdx.y;
+    float mx = 0.f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float *x = P + ((int64_t)j * n + i) * sub;
+        double ss = 0.0;
+        for (int t = 0; t < sub; ++t) ss = fma((double)x[t], (double)x[t], ss);
+        const float r = __double2float_ru(sqrt(ss) * (1.0 + 1e-12));
+        mx = (r != r || r > mx) ? r : mx;
+    }
+    // non-negative floats order like their bits; a NaN (bits above +inf) poisons the guard
+    unsigned bits = __float_as_uint(mx);
+    for (int o = 16; o; o >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(rmax + j, bits);
+}
+
+__global__ void final_guard_kernel(float *__restrict__ guard, const unsigned *__restrict__ rmax, int m, int sub, float kE) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const double u = 1.0 / 16777216.0;
+    const double g = (sub + 4) * u / (1.0 - (sub + 4) * u);
+    const double g0 = guard[2 * j], g1 = guard[2 * j + 1], R = __uint_as_float(rmax[j]);
+    guard[2 * j] = __double2float_ru(g0 * (1.0 + (u + g) / kE) * (1.0 + 1e-6));
+    guard[2 * j + 1] = __double2float_ru((g1 * (1.0 + g / kE) + g * R / (2.0 * kE)) * (1.0 + 1e-6));
+}
+
+template <int SUBC>  // k == 256
+__global__ void __launch_bounds__(256)
+final_settle_kernel(const float *__restrict__ P, int64_t n, const float *__restrict__ C32,
+                    const uint8_t *__restrict__ codes, const uint8_t *__restrict__ flags, int32_t *__restrict__ assign) {
+    const int j = blockIdx.y;
+    constexpr int kCS = SUBC + 1;  // padded centroid stride (per-lane centroids spread over the banks)
+    __shared__ float sC[256 * kCS], scc[256];
+    for (int q = threadIdx.x; q < 256 * SUBC; q += blockDim.x) sC[(q / SUBC) * kCS + q % SUBC] = C32[(int64_t)j * 256 * SUBC + q];
+    __syncthreads();
+    for (int l = threadIdx.x; l < 256; l += blockDim.x) {  // cc_l: the reference's sequential chain
+        float cc = 0.f;
+#pragma unroll
+        for (int t = 0; t < SUBC; ++t) cc = __fadd_rn(cc, __fmul_rn(sC[l * kCS + t], sC[l * kCS + t]));
+        scc[l] = cc;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - lane < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const bool ok = i < n;
+        const int64_t ji = (int64_t)j * n + (ok ? i : 0);
+        const bool fl = ok && flags[ji] != 0;
+        if (ok && !fl) assign[ji] = codes[ji];
+        unsigned todo = __ballot_sync(0xffffffffu, fl);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int64_t jf = (int64_t)j * n + (i - lane + src);
+            float x[SUBC];
+            const float4 *xp = reinterpret_cast<const float4 *>(P + jf * SUBC);
+#pragma unroll
+            for (int q = 0; q < SUBC / 4; ++q) {
+                const float4 v = xp[q];
+                x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+            }
+            float vv = 0.f;
+#pragma unroll
+            for (int t = 0; t < SUBC; ++t) vv = __fadd_rn(vv, __fmul_rn(x[t], x[t]));
+            float bd = __int_as_float(0x7f800000);
+            int bl = -1;
+#pragma unroll 1
+            for (int r = 0; r < 8; ++r) {  // centroids lane + 32 r, ascending: strict < keeps the first
+                const int l = lane + 32 * r;
+                float dd = 0.f;
+#pragma unroll
+                for (int t = 0; t < SUBC; ++t) dd = __fadd_rn(dd, __fmul_rn(x[t], sC[l * kCS + t]));
+                const float d1 = __fsub_rn(__fadd_rn(vv, scc[l]), __fmul_rn(2.0f, dd));
+                if (d1 < bd) { bd = d1; bl = l; }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const float od = __shfl_xor_sync(0xffffffffu, bd, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                if (ol >= 0 && (bl < 0 || od < bd || (od == bd && ol < bl))) { bd = od; bl = ol; }
+            }
+            if (lane == 0) assign[jf] = bl < 0 ? 0 : bl;  // nothing below +inf: index 0 (best = inf)
+        }
+    }
+}
+
+__global__ void final_bias_kernel(const float *__restrict__ C32, int64_t mk, int sub, float *__restrict__ b32) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= mk) return;
+    double ss = 0.0;  // float products are exact in float64: b = |c|^2 / 2 rounded once (to within u b)
+    for (int t = 0; t < sub; ++t) ss = fma((double)C32[i * sub + t], (double)C32[i * sub + t], ss);
+    b32[i] = __double2float_rn(0.5 * ss);
+}
+
+static bool tc_screen_ok(const float *P, int m, int sub, int k) {
+    const char *tcv = getenv("CSPQ_LLOYD_TC");  // "0": the plain kernels (A/B and tests)
+    return !(tcv && tcv[0] == '0') && k == 256 && (sub == 4 || sub == 8) && reinterpret_cast<uintptr_t>(P) % 16 == 0 &&
+           m <= encode_tc_max_subspaces(sub, CSPQ_IN_F32);
+}
+
+static int final_assign_tc(const float *P32, int64_t n, int m, int sub, int k, const float *C32, int32_t *assign, void *ws,
+                           const WsLayout &L, cudaStream_t st) {
+    float *b32 = L.at<float>(ws, L.tc_b), *guard = L.at<float>(ws, L.tc_guard);
+    void *img = L.at<void>(ws, L.tc_img);
+    uint8_t *codes = L.at<uint8_t>(ws, L.tc_codes), *flags = L.at<uint8_t>(ws, L.tc_flags);
+    unsigned *rmax = L.at<unsigned>(ws, L.tc_rmax);
+    int rc;
+    final_bias_kernel<<<(unsigned)(((int64_t)m * k + 255) / 256), 256, 0, st>>>(C32, (int64_t)m * k, sub, b32);
+    CSPQ_LAUNCH_CHECK();
+    if ((rc = encode_prepare(C32, b32, m, k, sub, guard, st))) return rc;
+    CSPQ_CUDA_TRY(cudaMemsetAsync(rmax, 0, sizeof(unsigned) * m, st));
+    dim3 gn((unsigned)grid_for(n, 256, std::max<int64_t>(1, 148 * 4 / m)), (unsigned)m);
+    pnorm_max_kernel<<<gn, 256, 0, st>>>(P32, n, sub, rmax);
+    CSPQ_LAUNCH_CHECK();
+    final_guard_kernel<<<(m + 127) / 128, 128, 0, st>>>(guard, rmax, m, sub, encode_tc_error_constant(sub));
+    CSPQ_LAUNCH_CHECK();
+    if ((rc = encode_tc_prepare(C32, b32, m, k, sub, img, st))) return rc;
+    if ((rc = encode_tc_ex(P32, CSPQ_IN_F32, n, sub, n * sub, C32, b32, guard, img, m, k, sub, codes, 1, n, flags, nullptr, st)))
+        return rc;
+    dim3 grid((unsigned)grid_for(n, 256, std::max<int64_t>(1, 148 * 8 / m)), (unsigned)m);
+    if (sub == 8) final_settle_kernel<8><<<grid, 256, 0, st>>>(P32, n, C32, codes, flags, assign);
+    else final_settle_kernel<4><<<grid, 256, 0, st>>>(P32, n, C32, codes, flags, assign);
+    CSPQ_LAUNCH_CHECK();
+    return CSPQ_OK;
+}
+
 int lloyd_assign(const void *P, int pf64, int64_t n, int m, int sub, int k, const double *C64,
                  const int32_t *state, int64_t b, int64_t e, int32_t *assign, double *sq, void *ws, cudaStream_t st) {
     WsLayout L(n, m, sub, k);
@@ -999,10 +1136,7 @@ int lloyd_assign(const void *P, int pf64, int64_t n, int m, int sub, int k, cons
     cnorm_kernel<<<(unsigned)((mk + 255) / 256), 256, 0, st>>>(C64, m, k, sub, state, cn);
     CSPQ_LAUNCH_CHECK();
     if (e <= b) return CSPQ_OK;
-    const char *tcv = getenv("CSPQ_LLOYD_TC");  // "0": the plain float64 kernel (A/B and tests)
-    const bool tc_on = !(tcv && tcv[0] == '0');
-    if (tc_on && !pf64 && k == 256 && (sub == 4 || sub == 8) && reinterpret_cast<uintptr_t>(P) % 16 == 0 &&
-        m <= encode_tc_max_subspaces(sub, CSPQ_IN_F32))
+    if (!pf64 && tc_screen_ok(reinterpret_cast<const float *>(P), m, sub, k))
         return assign_tc(reinterpret_cast<const float *>(P), n, m, sub, k, C64, cn, state, b, e, assign, sq, ws, L, st);
     const size_t need = (size_t)k * (sub + 1) * sizeof(double);
     const int use_smem = need <= 96 * 1024;
@@ -1131,7 +1265,11 @@ int lloyd_train(const void *P, int pf64, int64_t n, int m, int sub, int k, doubl
         CSPQ_LAUNCH_CHECK();
         P32 = p32;
     }
-    if ((rc = encode_subspace_major(P32, n, m, sub, C32, nullptr, k, assign, CSPQ_VARIANT_REFERENCE, st))) return rc;
+    if (tc_screen_ok(P32, m, sub, k)) {
+        if ((rc = final_assign_tc(P32, n, m, sub, k, C32, assign, ws, L, st))) return rc;
+    } else if ((rc = encode_subspace_major(P32, n, m, sub, C32, nullptr, k, assign, CSPQ_VARIANT_REFERENCE, st))) {
+        return rc;
+    }
     if ((rc = lloyd_final_objective(P, pf64, n, m, sub, k, C32, assign, obj, ws, st))) return rc;
     write_final_obj_kernel<<<(m + 127) / 128, 128, 0, st>>>(obj, m, max_iters, iterations, objectives);
     CSPQ_LAUNCH_CHECK();

@@ -249,6 +249,32 @@ def test_tensor_screened_assignment_ties(P, monkeypatch, oracle):
         o = oracle.lloyd(pts[j].astype(np.float64), init[j], 6, 0.0)
         assert got[j].centroids.tobytes() == o["centroids"].tobytes()
         assert got[j].objectives == o["objectives"]
+        assert np.array_equal(got[j].assignments, o["assignments"])
+
+
+@pytest.mark.parametrize("sub", [4, 8])
+def test_screened_final_pass_far_from_origin(P, monkeypatch, oracle, sub):
+    """The final float32 REFERENCE pass (training.py:143-150) is screened by
+    the tensor kernel with a band widened for the REFERENCE's own rounding:
+    points far from the origin make |x|^2 dominate (vv + cc_l) - 2 dd_l, so
+    the REFERENCE rounds many real gaps away (exact ties and swapped orders);
+    every such point must be flagged and rescanned.  Final assignments and
+    objectives equal the plain REFERENCE kernel's and the oracle's."""
+    rng = np.random.default_rng(11 + sub)
+    m, n, k = 3, 20_000, 256
+    pts = (1000.0 + rng.standard_normal((m, n, sub)) * np.array([0.5, 2.0, 8.0])[:, None, None]).astype(np.float32)
+    init = np.ascontiguousarray(pts[:, rng.choice(n, k, replace=False)].astype(np.float64))
+    cfg = P.TrainConfig(k=k, max_iters=3, tol=0.0)
+    monkeypatch.setenv("CSPQ_LLOYD_TC", "0")
+    ref = P.lloyd_iterate_batched(pts, init, cfg)
+    monkeypatch.setenv("CSPQ_LLOYD_TC", "1")
+    got = P.lloyd_iterate_batched(pts, init, cfg)
+    for j in range(m):
+        assert np.array_equal(got[j].assignments, ref[j].assignments), j
+        assert got[j].objectives == ref[j].objectives
+        o = oracle.lloyd(pts[j].astype(np.float64), init[j], 3, 0.0)
+        assert np.array_equal(got[j].assignments, o["assignments"]), j
+        assert got[j].objectives == o["objectives"]
 
 
 def test_screened_assignment_on_row_ranges(P, monkeypatch):
