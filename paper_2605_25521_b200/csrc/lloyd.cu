@@ -553,9 +553,18 @@ __global__ void scan_kernel(int32_t *__restrict__ hist, int k, int64_t nch, cons
     const int j = blockIdx.x;
     if (!state[j]) return;
     int32_t *H = hist + (int64_t)j * nch * k;
+    constexpr int kU = 16;  // chunk counts loaded kU at a time: independent loads, one latency per batch
     for (int l = threadIdx.x; l < k; l += blockDim.x) {
         int32_t run = 0;
-        for (int64_t c = 0; c < nch; ++c) {
+        int64_t c = 0;
+        for (; c + kU <= nch; c += kU) {
+            int32_t v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) v[u] = H[(c + u) * k + l];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) { H[(c + u) * k + l] = run; run += v[u]; }
+        }
+        for (; c < nch; ++c) {
             const int32_t v = H[c * k + l];
             H[c * k + l] = run;
             run += v;
@@ -585,35 +594,48 @@ __global__ void scan_kernel(int32_t *__restrict__ hist, int k, int64_t nch, cons
         if (threadIdx.x == blockDim.x - 1) carry += s[threadIdx.x];
         __syncthreads();
     }
-    for (int l = threadIdx.x; l < k; l += blockDim.x) {
-        const int32_t st = start[(int64_t)j * k + l];
-        for (int64_t c = 0; c < nch; ++c) H[c * k + l] += st;
-    }
+    // (the bin starts are added to the chunk offsets by scatter_kernel)
 }
 
 // stable scatter: perm[j][pos] = i, in ascending i within each cluster
 __global__ void scatter_kernel(const int32_t *__restrict__ assign, int64_t n, int k, const int32_t *state,
                                int64_t b, int64_t e, int64_t nch, int32_t *__restrict__ hist,
-                               int32_t *__restrict__ perm) {
+                               const int32_t *__restrict__ start, int32_t *__restrict__ perm, int use_smem) {
     const int j = blockIdx.y;
     if (!state[j]) return;
     const int64_t c = blockIdx.x;
     const int lane = threadIdx.x;
-    int32_t *run = hist + ((int64_t)j * nch + c) * k;
+    // running positions = bin start + this chunk's offset within the bin, in shared memory when
+    // k fits (the read-modify-write per 32 points is then not a global-memory round trip)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int32_t *H = hist + ((int64_t)j * nch + c) * k;
+    int32_t *run = use_smem ? reinterpret_cast<int32_t *>(smem_raw) : H;
+    for (int q = lane; q < k; q += 32) run[q] = H[q] + start[(int64_t)j * k + q];
+    __syncwarp();
     const int64_t lo = b + c * kChunk, hi = min(e, lo + kChunk);
     const unsigned lt = (1u << lane) - 1u;
-    for (int64_t base = lo; base < hi; base += 32) {
-        const int64_t i = base + lane;
-        const int a = i < hi ? assign[(int64_t)j * n + i] : -1 - lane;  // unique sentinels never match
-        const unsigned peers = __match_any_sync(0xffffffffu, a);
-        if (a >= 0) {
-            const int rank = __popc(peers & lt);
-            const int32_t pos = run[a] + rank;
-            perm[(int64_t)j * n + pos] = (int32_t)(i - b);
+    constexpr int kB = 8;  // assignments of 8 x 32 points loaded ahead (independent loads)
+    for (int64_t base0 = lo; base0 < hi; base0 += 32 * kB) {
+        int av[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int64_t i = base0 + 32 * u + lane;
+            av[u] = i < hi ? assign[(int64_t)j * n + i] : -1 - lane;  // unique sentinels never match
         }
-        __syncwarp();
-        if (a >= 0 && lane == __ffs(peers) - 1) run[a] += __popc(peers);
-        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const int64_t i = base0 + 32 * u + lane;
+            const int a = av[u];
+            const unsigned peers = __match_any_sync(0xffffffffu, a);
+            if (a >= 0) {
+                const int rank = __popc(peers & lt);
+                const int32_t pos = run[a] + rank;
+                perm[(int64_t)j * n + pos] = (int32_t)(i - b);
+            }
+            __syncwarp();
+            if (a >= 0 && lane == __ffs(peers) - 1) run[a] += __popc(peers);
+            __syncwarp();
+        }
     }
 }
 
@@ -1179,7 +1201,9 @@ int lloyd_accumulate(const void *P, int pf64, int64_t n, int m, int sub, int k, 
     scan_kernel<<<m, 256, 0, st>>>(hist, k, nch, state, cnt, start, counts);
     CSPQ_LAUNCH_CHECK();
     if (nch > 0) {
-        scatter_kernel<<<dim3((unsigned)nch, (unsigned)m), 32, 0, st>>>(assign, n, k, state, b, e, nch, hist, perm);
+        const int use_smem = (size_t)k * 4 <= 48 * 1024;
+        scatter_kernel<<<dim3((unsigned)nch, (unsigned)m), 32, use_smem ? k * 4 : 0, st>>>(assign, n, k, state, b, e, nch,
+                                                                                          hist, start, perm, use_smem);
         CSPQ_LAUNCH_CHECK();
     }
     const int64_t tot = (int64_t)m * k * sub;
