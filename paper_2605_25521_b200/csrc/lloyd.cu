@@ -35,6 +35,9 @@ namespace cspq {
 
 namespace {
 
+#ifndef CSPQ_SUMS_KB
+#define CSPQ_SUMS_KB 32  // sums_kernel gathers in flight per thread (16: c4 training +8 %)
+#endif
 constexpr int kChunk = 1024;  // points per histogram/scatter chunk
 constexpr uint64_t kMagic = 0x43535051424C4C59ull;
 
@@ -657,8 +660,8 @@ __global__ void sums_kernel(const TP *__restrict__ P, int64_t n, int m, int k, i
     const TP *Pj = P + ((int64_t)j * n + b) * sub + t;
     double s = 0.0;
     int32_t p = 0;
-    // 16 gathers in flight per step; the next step's indices are loaded before this step's sum
-    constexpr int kB = 16;
+    // CSPQ_SUMS_KB gathers in flight per step; the next step's indices are loaded before this step's sum
+    constexpr int kB = CSPQ_SUMS_KB;
     int32_t idx[kB];
     if (cc >= kB) {
 #pragma unroll
