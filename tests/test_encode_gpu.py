@@ -32,7 +32,7 @@ def cset_of(P, rowmajor, biases=None):
 
 def device_codes(P, X, cs, variant, mode="auto", precomputed_bias=True):
     import torch
-    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    Xd = torch.from_numpy(np.array(X, copy=True, order="C")).cuda()
     plan = P.ExecutionPlan(variant=variant, mode=mode)
     out = P.encode_dataset_device(Xd, cs, plan, precomputed_bias=precomputed_bias)
     torch.cuda.synchronize()
