@@ -13,10 +13,12 @@
 //   buffers so the MMA of tile t+1 overlaps the epilogue of tile t;
 //   epilogue warps read their rows with tcgen05.ld (64 columns per load) and
 //   run an argmin that also finds the runner-up exactly without re-reading
-//   anything: blocks of 8 centroids give block minima (FMNMX3) and a running
-//   best/runner-up over blocks; eight "class" minima (centroid index mod 8)
-//   catch a runner-up that shares the winner's block, because a block and a
-//   class intersect in exactly one centroid.  The code is 8*block + class.
+//   anything: every 16 centroids form a block of 7 and a block of 9 (three-
+//   input minima with no idle operand: 3 + 4 FMNMX3), 32 block minima in all;
+//   nine "class" minima (position inside the block) catch a runner-up that
+//   shares the winner's block, because a block and a class intersect in at
+//   most one centroid.  Block slot s starts at centroid 8s - (s & 1); the
+//   code is that start + class.
 //   A (row, subspace) whose runner-up lies within the error band of the
 //   tensor-core score is re-encoded exactly by its warp (strict fp32 chains,
 //   warp-shuffle argmin) -- the same fix-up as the SIMT kernel.
@@ -59,6 +61,7 @@ namespace {
 
 constexpr int kTM = 128;     // rows per tile (MMA M)
 constexpr int kN = 256;      // centroids (MMA N)
+constexpr int kNCls = 9;     // argmin classes = position inside a block of 7 or 9 centroids
 constexpr int kG = 8;        // max tiles per row group (codebook image reuse); the launch picks 1..kG
 constexpr int kGroups = 3;   // epilogue groups: item it belongs to group it % kGroups
 constexpr int kNA = kGroups; // A-operand stages (a group writes item it + kGroups into item it's stage)
@@ -485,9 +488,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
             const int j = ii.j;
-            float cls[8];
+            float cls[kNCls];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) cls[c] = pos_inf_f();
+            for (int c = 0; c < kNCls; ++c) cls[c] = pos_inf_f();
 #pragma unroll
             for (int ch = 0; ch < 4 && !(probe & 1); ++ch) {
                 constexpr int kLdPerChunk = kCW / 64;
@@ -508,17 +511,22 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                     cls[ch] = __fadd_rn(SV(0), SV(63));
                     continue;
                 }
+                // each 16 columns = a block of 7 then a block of 9 (3 + 4 three-input minima, no
+                // idle operand slot); the class is the position inside the block, so classes 0-6
+                // take two columns per 16 and classes 7-8 one (paired across 16-column groups)
                 float bmc[8];
 #pragma unroll
                 for (int bp = 0; bp < 4; ++bp) {
+                    const int o = 16 * bp;
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) cls[c] = fmin3(cls[c], SV(16 * bp + c), SV(16 * bp + 8 + c));
-#pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const int o = 16 * bp + 8 * hh;
-                        bmc[2 * bp + hh] = fmin3(fmin3(SV(o), SV(o + 1), SV(o + 2)), fmin3(SV(o + 3), SV(o + 4), SV(o + 5)),
-                                                 fminf(SV(o + 6), SV(o + 7)));
+                    for (int c = 0; c < 7; ++c) cls[c] = fmin3(cls[c], SV(o + c), SV(o + 7 + c));
+                    if (bp & 1) {
+                        cls[7] = fmin3(cls[7], SV(o - 2), SV(o + 14));
+                        cls[8] = fmin3(cls[8], SV(o - 1), SV(o + 15));
                     }
+                    bmc[2 * bp] = fmin3(fmin3(SV(o), SV(o + 1), SV(o + 2)), fmin3(SV(o + 3), SV(o + 4), SV(o + 5)), SV(o + 6));
+                    bmc[2 * bp + 1] = fmin3(fmin3(SV(o + 7), SV(o + 8), SV(o + 9)), fmin3(SV(o + 10), SV(o + 11), SV(o + 12)),
+                                            fmin3(SV(o + 13), SV(o + 14), SV(o + 15)));
                 }
                 reinterpret_cast<float4 *>(scratch + 8 * ch)[0] = make_float4(bmc[0], bmc[1], bmc[2], bmc[3]);
                 reinterpret_cast<float4 *>(scratch + 8 * ch)[1] = make_float4(bmc[4], bmc[5], bmc[6], bmc[7]);
@@ -562,13 +570,13 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             // -- and the indicator-weighted index sums give the winner's block and class exactly.
             // (An indicator < 2^-24 can vanish in a sum; its value is > 3.9 E W from m1, outside
             // the 2 E W that exactness needs.)
-            const float m1 = fmin3(fmin3(cls[0], cls[1], cls[2]), fmin3(cls[3], cls[4], cls[5]), fminf(cls[6], cls[7]));
+            const float m1 = fmin3(fmin3(cls[0], cls[1], cls[2]), fmin3(cls[3], cls[4], cls[5]), fmin3(cls[6], cls[7], cls[8]));
             const float W = sGuard[2 * j] + xnorm * sGuard[2 * j + 1];
             float kinv;
             asm("rcp.approx.f32 %0, %1;" : "=f"(kinv) : "f"(4.0f * kE * W));  // inf for W = 0: every ind = 0 (flag)
             float qcf = 0.f, ncf = 0.f, wbf = 0.f, nbf = 0.f;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
+            for (int c = 0; c < kNCls; ++c) {
                 const float ind = __saturatef(__fmaf_rn(__fsub_rn(cls[c], m1), -kinv, 1.0f));
                 qcf = __fmaf_rn(ind, (float)(c + 8), qcf);
                 ncf = __fadd_rn(ncf, ind);
@@ -580,7 +588,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 nbf = __fadd_rn(nbf, ind);
             }
             const int64_t row = ii.tile() * kTM + r;
-            int code = 8 * (__float2int_rz(wbf) - 32) + (__float2int_rz(qcf) - 8);
+            // block slot sb starts at column 8 sb - (sb & 1) (7-blocks at even slots, 9-blocks at odd)
+            const int sb = __float2int_rz(wbf) - 32;
+            int code = 8 * sb - (sb & 1) + (__float2int_rz(qcf) - 8);
             const bool flag = (row < n) && !(ncf == 1.0f && nbf == 1.0f);
             // exact warp-cooperative re-encode of flagged rows (x and the fp32 codebook from
             // shared memory: the item's x slot stays valid until kPD more owned items)
