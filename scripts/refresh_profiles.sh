@@ -14,6 +14,6 @@ echo "ref rc=$?" >> gpurun_out/${tag}_status.txt
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${tag}_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_ncu_launch.log 2>&1
 echo "ncu launches rc=$?" >> gpurun_out/${tag}_status.txt
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:encode_tc_kernel --launch-skip 12 -c 1 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:encode_tc_kernel --launch-skip 13 -c 1 \
   -o gpurun_out/${tag}_tc_full python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_ncu_full.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/${tag}_status.txt

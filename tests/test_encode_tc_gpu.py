@@ -178,3 +178,28 @@ def test_too_many_subspaces_for_tensor_kernel(P, oracle):
     init = np.ascontiguousarray(np.repeat(pts[:, :1], 256, axis=1).astype(np.float64) + rm.astype(np.float64))
     res = P.lloyd_iterate_batched(pts, init, P.TrainConfig(k=256, max_iters=2, tol=0.0))
     assert len(res) == m and all(r.iterations >= 1 for r in res)
+
+
+@pytest.mark.parametrize("sub", [8, 4])
+def test_every_centroid_index_decodes_tensor(P, oracle, sub):
+    """Each row equals one centroid per subspace, so every index 0..255 wins
+    once in every subspace: checks the block-slot/class -> code mapping of the
+    epilogue (blocks of 7 and 9, slot s starts at 8 s - (s & 1)) on decided
+    rows, and duplicated centroids inside one block and across blocks take the
+    fix-up (lowest index wins, as in the oracle)."""
+    rng = np.random.default_rng(5 + sub)
+    m, k = 3, 256
+    rm = (4.0 * rng.standard_normal((m, k, sub))).astype(np.float32)
+    idx = (np.arange(k)[:, None] + 37 * np.arange(m)[None, :]) % k
+    X = np.stack([rm[j, idx[:, j]] for j in range(m)], axis=1).reshape(k, m * sub)
+    cs = cset_of(P, rm)
+    got = tc_codes(P, X, cs)
+    assert (got == idx.astype(np.uint8)).all()
+    assert got.tobytes() == oracle.encode(X, cs.rowmajor, cs.biases, oracle.VARIANT_REFORM).tobytes()
+    dup = rm.copy()
+    for a, b in [(0, 6), (7, 15), (14, 15), (16, 31), (6, 7), (250, 255), (100, 228)]:
+        dup[:, b] = dup[:, a]
+    cs2 = cset_of(P, dup)
+    X2 = np.stack([dup[j, idx[:, j]] for j in range(m)], axis=1).reshape(k, m * sub)
+    assert tc_codes(P, X2, cs2).tobytes() == oracle.encode(X2, cs2.rowmajor, cs2.biases,
+                                                           oracle.VARIANT_REFORM).tobytes()
