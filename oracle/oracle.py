@@ -54,6 +54,8 @@ def lib():
         L.oracle_lloyd.restype = i32
         L.oracle_pairwise_sum.argtypes = [vp, i64]
         L.oracle_pairwise_sum.restype = ctypes.c_double
+        L.oracle_einsum_dot.argtypes = [vp, vp, i32]
+        L.oracle_einsum_dot.restype = ctypes.c_double
         _lib = L
     return _lib
 
@@ -114,6 +116,13 @@ def lloyd(pts64, init64, max_iters: int, tol: float, threads: int = 0):
 def pairwise_sum(a) -> float:
     a = np.ascontiguousarray(a, dtype=np.float64)
     return float(lib().oracle_pairwise_sum(_ptr(a), a.shape[0]))
+
+
+def einsum_dot(a, b) -> float:
+    """np.einsum("t,t->") order for one float64 row pair (oracle_einsum_dot)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return float(lib().oracle_einsum_dot(_ptr(a), _ptr(b), a.shape[0]))
 
 
 def compute_biases(rowmajor) -> np.ndarray:

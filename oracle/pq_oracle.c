@@ -36,8 +36,10 @@
  *
  * Parity pin: tests/test_oracle_golden.py checks every routine here against
  * golden vectors produced by importing the reference itself
- * (tests/golden/make_golden.py).  Encode is bit-exact; Lloyd matches to the
- * tolerance BLAS/einsum summation order allows.
+ * (tests/golden/make_golden.py).  Encode is bit-exact; the float64 squared
+ * norms follow np.einsum's own order (oracle_einsum_dot), so Lloyd differs
+ * from the reference only where OpenBLAS's dgemm order would differ from the
+ * ascending fused chain (none observed).
  *
  * Build: oracle/Makefile (gcc -O3 -fopenmp -ffp-contract=off; the clones are
  * vectorised across centroids only, which never reorders a centroid's own
@@ -194,6 +196,30 @@ int oracle_encode(const void *X, int in_u8, int64_t n, int d, const float *CB, c
 /* float64 helpers for Lloyd                                                */
 /* ------------------------------------------------------------------------ */
 
+/* np.einsum("it,it->i") / ("kt,kt->k") on contiguous float64 rows of length n
+ * (training.py:61/70/88/134/154, core.py via the same routine): numpy's
+ * sum_of_products_contig_contig_outstride0_two with 2-lane (SSE2 baseline)
+ * vectors.  Each 8-element block is folded into the two lane accumulators
+ * back to front (acc = p[t+L] + (p[t+2+L] + (p[t+4+L] + (p[t+6+L] + acc))),
+ * npyv_muladd without FMA = product rounded, then added), the tail adds one
+ * lane pair at a time, and the result is lane0 + lane1.  Checked bit-exact
+ * against np.einsum for n = 1..24 (tests/test_oracle_golden.py). */
+double oracle_einsum_dot(const double *a, const double *b, int n) {
+    double l0 = 0.0, l1 = 0.0;
+    int t = 0;
+    for (; n - t >= 8; t += 8) {
+        l0 = a[t + 6] * b[t + 6] + l0; l1 = a[t + 7] * b[t + 7] + l1;
+        l0 = a[t + 4] * b[t + 4] + l0; l1 = a[t + 5] * b[t + 5] + l1;
+        l0 = a[t + 2] * b[t + 2] + l0; l1 = a[t + 3] * b[t + 3] + l1;
+        l0 = a[t] * b[t] + l0;         l1 = a[t + 1] * b[t + 1] + l1;
+    }
+    for (; t < n; t += 2) {
+        l0 = a[t] * b[t] + l0;
+        if (t + 1 < n) l1 = a[t + 1] * b[t + 1] + l1;
+    }
+    return l0 + l1;
+}
+
 /* numpy's pairwise summation for a contiguous float64 array (what
  * ndarray.sum() does for training.py:73/154): <8 sequential, <=128 eight
  * accumulators, else split at n/2 rounded down to a multiple of 8. */
@@ -240,9 +266,7 @@ static void lloyd_assign_rows(const double *P, int64_t i0, int64_t i1, int sub, 
             double dl = cn[l] - 2.0 * dot[l];
             if (dl < best) { best = dl; bi = l; }
         }
-        double xx = 0.0;
-        for (int t = 0; t < sub; ++t) xx += x[t] * x[t];
-        double v = best + xx;
+        double v = best + oracle_einsum_dot(x, x, sub);
         assign[i] = bi;
         sq[i] = v > 0.0 ? v : 0.0;
     }
@@ -252,12 +276,8 @@ static double lloyd_assign(const double *P, int64_t n, int sub, const double *C,
                            int64_t *assign, double *sq, double *cn) {
     double *CT = (double *)malloc(sizeof(double) * (size_t)k * sub);
     for (int l = 0; l < k; ++l) {
-        double s = 0.0;
-        for (int t = 0; t < sub; ++t) {
-            s += C[(int64_t)l * sub + t] * C[(int64_t)l * sub + t];
-            CT[(int64_t)t * k + l] = C[(int64_t)l * sub + t];
-        }
-        cn[l] = s;
+        for (int t = 0; t < sub; ++t) CT[(int64_t)t * k + l] = C[(int64_t)l * sub + t];
+        cn[l] = oracle_einsum_dot(C + (int64_t)l * sub, C + (int64_t)l * sub, sub);
     }
     const int64_t ROWS = 1024;
 #pragma omp parallel
@@ -312,14 +332,12 @@ int oracle_lloyd(const double *P, int64_t n, int sub, double *C, int k, int max_
             }
         }
         if (nempty) { /* training.py:129-136 */
+            double *df = (double *)malloc(sizeof(double) * (size_t)sub);
             for (int64_t i = 0; i < n; ++i) {
-                double r = 0.0;
-                for (int t = 0; t < sub; ++t) {
-                    double df = P[i * sub + t] - C[assign[i] * sub + t];
-                    r += df * df;
-                }
-                resid[i] = r;
+                for (int t = 0; t < sub; ++t) df[t] = P[i * sub + t] - C[assign[i] * sub + t];
+                resid[i] = oracle_einsum_dot(df, df, sub);
             }
+            free(df);
             for (int l = 0; l < k; ++l) {
                 if (counts[l] > 0) continue;
                 int64_t cand = 0;
@@ -338,14 +356,12 @@ int oracle_lloyd(const double *P, int64_t n, int sub, double *C, int k, int max_
     for (int64_t q = 0; q < n * sub; ++q) p32[q] = (float)P[q];
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) assign_out[i] = ref_one(p32 + i * sub, cast_out, k, sub, NULL);
+    double *df = (double *)malloc(sizeof(double) * (size_t)sub);
     for (int64_t i = 0; i < n; ++i) {
-        double r = 0.0;
-        for (int t = 0; t < sub; ++t) {
-            double df = P[i * sub + t] - (double)cast_out[assign_out[i] * sub + t];
-            r += df * df;
-        }
-        sq[i] = r;
+        for (int t = 0; t < sub; ++t) df[t] = P[i * sub + t] - (double)cast_out[assign_out[i] * sub + t];
+        sq[i] = oracle_einsum_dot(df, df, sub);
     }
+    free(df);
     objectives[nobj++] = oracle_pairwise_sum(sq, n);
     *iters_out = iters;
     free(p32); free(assign); free(sq); free(cn); free(sums); free(counts); free(resid);

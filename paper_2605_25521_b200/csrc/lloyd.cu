@@ -5,7 +5,7 @@
 // subspaces instead of the reference's sequential subspace loop
 // (training.py:212-223).  Arithmetic follows the oracle (oracle/pq_oracle.c)
 // operation for operation so GPU and oracle agree bit for bit:
-//   * assignment: ||c||^2 as a sequential mul-then-add sum, x.c as an
+//   * assignment: ||c||^2 in np.einsum's order (einsum_sum), x.c as an
 //     ascending fused chain (a dgemm micro-kernel's rank-1 order),
 //     d = ||c||^2 - 2 x.c, argmin first index (np.argmin);
 //   * objective terms sq = np.maximum(d_min + ||x||^2, 0) and their sum in
@@ -285,6 +285,29 @@ __global__ void combine_levels_kernel(int m, const int32_t *state, const double 
     if (threadIdx.x == 0) out[j] = nv[off[H] - 1];  // the root is alone on the top level
 }
 
+// ---------------------------------------------------------------- einsum order
+// np.einsum("it,it->i") on contiguous float64 rows (training.py:61/70/88/134/154): numpy's
+// sum_of_products_contig_contig_outstride0_two with 2-lane vectors -- every 8-element block
+// folded back to front into two lane accumulators (product rounded, then added), a tail of lane
+// pairs, then lane0 + lane1.  prod(t) returns the rounded product of element t.  Same order as
+// oracle_einsum_dot (oracle/pq_oracle.c); with n a compile-time constant it unrolls completely.
+template <typename G>
+__device__ __forceinline__ double einsum_sum(G prod, int n) {
+    double l0 = 0.0, l1 = 0.0;
+    int t = 0;
+    for (; n - t >= 8; t += 8) {
+        l0 = __dadd_rn(prod(t + 6), l0); l1 = __dadd_rn(prod(t + 7), l1);
+        l0 = __dadd_rn(prod(t + 4), l0); l1 = __dadd_rn(prod(t + 5), l1);
+        l0 = __dadd_rn(prod(t + 2), l0); l1 = __dadd_rn(prod(t + 3), l1);
+        l0 = __dadd_rn(prod(t), l0);     l1 = __dadd_rn(prod(t + 1), l1);
+    }
+    for (; t < n; t += 2) {
+        l0 = __dadd_rn(prod(t), l0);
+        if (t + 1 < n) l1 = __dadd_rn(prod(t + 1), l1);
+    }
+    return __dadd_rn(l0, l1);
+}
+
 // ---------------------------------------------------------------- assignment
 #ifndef CSPQ_LLOYD_PPT
 #define CSPQ_LLOYD_PPT 4  // points per thread in assign_kernel (2x4, 4x2, 4x4, 2x8, 1x8 measured: 4x2 best)
@@ -298,9 +321,7 @@ __global__ void cnorm_kernel(const double *C64, int m, int k, int sub, const int
     const int j = (int)(i / k);
     if (state && !state[j]) return;
     const double *c = C64 + i * sub;
-    double s = 0.0;
-    for (int t = 0; t < sub; ++t) s = __dadd_rn(s, __dmul_rn(c[t], c[t]));
-    cn[i] = s;
+    cn[i] = einsum_sum([&](int t) { return __dmul_rn(c[t], c[t]); }, sub);  // c_norms, training.py:61
 }
 
 template <int SUBC, typename TP>
@@ -382,9 +403,7 @@ assign_kernel(const TP *__restrict__ P, int64_t n, int k, int sub_rt, const doub
             for (int p = 0; p < kPPT; ++p) {
                 const int64_t i = i0 + p;
                 if (i >= e) break;
-                double xx = 0.0;
-#pragma unroll
-                for (int t = 0; t < SUBC; ++t) xx = __dadd_rn(xx, __dmul_rn(x[p][t], x[p][t]));
+                const double xx = einsum_sum([&](int t) { return __dmul_rn(x[p][t], x[p][t]); }, SUBC);
                 const double v = __dadd_rn(best[p], xx);
                 assign[(int64_t)j * n + i] = bi[p];
                 sq[(int64_t)j * n + i] = (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(v, 0.0)
@@ -405,7 +424,7 @@ assign_kernel(const TP *__restrict__ P, int64_t n, int k, int sub_rt, const doub
                 const double dl = __dsub_rn(cnj[l], __dmul_rn(2.0, dot));
                 if (l == 0 || dl < best) { best = dl; bi = l; }
             }
-            for (int t = 0; t < sub; ++t) xx = __dadd_rn(xx, __dmul_rn((double)x[t], (double)x[t]));
+            xx = einsum_sum([&](int t) { return __dmul_rn((double)x[t], (double)x[t]); }, sub);
         }
         const double v = __dadd_rn(best, xx);
         assign[(int64_t)j * n + i] = bi;
@@ -486,9 +505,7 @@ tc_settle_kernel(const float *__restrict__ P, int64_t n, int k, const double *__
             fl[p] = ok[p] && flags[ji] != 0;
         }
         auto finish = [&](const double (&xv)[SUBC], int64_t ji, int l, double d) {
-            double xx = 0.0;
-#pragma unroll
-            for (int t = 0; t < SUBC; ++t) xx = __dadd_rn(xx, __dmul_rn(xv[t], xv[t]));
+            const double xx = einsum_sum([&](int t) { return __dmul_rn(xv[t], xv[t]); }, SUBC);
             const double v = __dadd_rn(d, xx);
             assign[ji] = l;
             sq[ji] = (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(v, 0.0)
@@ -734,12 +751,11 @@ repair_kernel(const TP *__restrict__ P, int64_t n, int k, int sub, const int32_t
     double *R = resid + (int64_t)j * n;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double *c = C + (int64_t)assign[(int64_t)j * n + i] * sub;
-        double r = 0.0;
-        for (int t = 0; t < sub; ++t) {
-            const double df = __dsub_rn((double)Pj[i * sub + t], c[t]);
-            r = __dadd_rn(r, __dmul_rn(df, df));
-        }
-        R[i] = r;
+        const TP *x = Pj + i * sub;
+        R[i] = einsum_sum([&](int t) {  // residual, training.py:133-134
+            const double df = __dsub_rn((double)x[t], c[t]);
+            return __dmul_rn(df, df);
+        }, sub);
     }
     __syncthreads();
     __shared__ double sv[1024];
@@ -816,12 +832,10 @@ __global__ void final_resid_kernel(const TP *__restrict__ P, int64_t n, int k, i
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const TP *x = P + ((int64_t)j * n + i) * sub;
         const float *c = C32 + ((int64_t)j * k + assign[(int64_t)j * n + i]) * sub;
-        double r = 0.0;
-        for (int t = 0; t < sub; ++t) {
+        out[(int64_t)j * n + i] = einsum_sum([&](int t) {  // final objective terms, training.py:153-154
             const double df = __dsub_rn((double)x[t], (double)c[t]);
-            r = __dadd_rn(r, __dmul_rn(df, df));
-        }
-        out[(int64_t)j * n + i] = r;
+            return __dmul_rn(df, df);
+        }, sub);
     }
 }
 
@@ -832,7 +846,7 @@ __global__ void write_final_obj_kernel(const double *obj, int m, int max_iters, 
 }
 
 // ---------------------------------------------------------------- k-means++ (training.py:76-92)
-// d2[i] = ||x_i - c||^2 (diff then sequential mul-add, like the oracle), or
+// d2[i] = ||x_i - c||^2 (diff, then np.einsum's order), or
 // min(d2[i], that) (np.minimum(d2, ., out=d2)).
 template <typename TP>
 __global__ void kpp_dist_kernel(const TP *__restrict__ P, int64_t n, int sub, const double *__restrict__ C64,
@@ -842,11 +856,10 @@ __global__ void kpp_dist_kernel(const TP *__restrict__ P, int64_t n, int sub, co
     const double *cen = C64 + ((int64_t)j * k + c) * sub;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const TP *x = P + ((int64_t)j * n + i) * sub;
-        double r = 0.0;
-        for (int t = 0; t < sub; ++t) {
+        const double r = einsum_sum([&](int t) {  // training.py:81/90
             const double df = __dsub_rn((double)x[t], cen[t]);
-            r = __dadd_rn(r, __dmul_rn(df, df));
-        }
+            return __dmul_rn(df, df);
+        }, sub);
         double *o = d2 + (int64_t)j * n + i;
         if (first) *o = r;
         else {

@@ -5,6 +5,9 @@ Run HERE (the container that has /root/reference), never on the GPU box:
 
     NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONPATH=/root/reference/pkg/src \
         python tests/golden/make_golden.py
+    # full-size Lloyd subspaces (samples dumped on the GPU box first):
+    gpurun -- python scripts/dump_train_samples.py
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py full gpurun_out/train_samples.npz
 
 It imports the reference package ``cspq`` (read-only, untouched) and records
 its outputs on small seeded inputs into ``tests/golden/*.npz``.  The inputs
@@ -351,7 +354,43 @@ def verify_cases():
     return out
 
 
+def full_lloyd_cases(training, samples_path):
+    """The reference's own lloyd_iterate (training.py:109-159, tol 0, the
+    config's sample-point init) on full-size training-sample subspaces of
+    BASELINE configs 2-5: c2 100K x 8 / 25 iterations, c3 200K x 8 / 10,
+    c4 1M x 4 / 20, c5 100K x 8 / 10.  The samples are generated on the GPU
+    (paper_2605_25521_b200/configs.py, Philox) and dumped by
+    scripts/dump_train_samples.py; only their SHA-256 is committed, and the
+    -m gpu test regenerates them and checks the hash before comparing."""
+    from paper_2605_25521_b200 import configs as C
+    S = np.load(samples_path)
+    out = {}
+    for key in sorted(k for k in S.files if k.endswith("/points")):
+        name, j, _ = key.split("/")
+        cfg = C.CONFIGS[name]
+        pts = S[key]
+        init = S[f"{name}/{j}/init"]
+        assert pts.shape == (cfg.n_train, cfg.sub) and init.shape == (cfg.k, cfg.sub)
+        tc = training.TrainConfig(k=cfg.k, max_iters=cfg.iters, tol=0.0)
+        r = training.lloyd_iterate(pts.astype(np.float64), init.astype(np.float64), tc)
+        g = f"{name}/{j}"
+        out[f"{g}/points_sha256"] = S[f"{g}/points_sha256"]
+        out[f"{g}/sample_sha256"] = S[f"{name}/sample_sha256"]
+        out[f"{g}/init"] = init
+        out[f"{g}/centroids"] = r.centroids
+        out[f"{g}/objectives"] = np.asarray(r.objectives, np.float64)
+        out[f"{g}/assignments"] = r.assignments.astype(np.uint8)  # k = 256
+        out[f"{g}/iterations"] = np.int64(r.iterations)
+        print(g, r.iterations, r.objectives[-1], flush=True)
+    return out
+
+
 def main():
+    if sys.argv[1:2] == ["full"]:  # full-size Lloyd goldens: make_golden.py full <train_samples.npz>
+        sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+        _, _, _, training = _ref()
+        np.savez_compressed(os.path.join(HERE, "lloyd_full_golden.npz"), **full_lloyd_cases(training, sys.argv[2]))
+        return
     bulk, core, kernels, training = _ref()
     if sys.argv[1:] == ["verify"]:  # (added later: regenerate only this archive)
         np.savez_compressed(os.path.join(HERE, "verify_golden.npz"), **verify_cases())

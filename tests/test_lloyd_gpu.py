@@ -33,6 +33,9 @@ def test_lloyd_vs_reference_golden(P, case):
     assert np.array_equal(r.assignments, g["assignments"])
     assert rel_err(r.centroids, g["centroids"]) <= 1e-5
     np.testing.assert_allclose(r.objectives, g["objectives"], rtol=1e-12, atol=1e-12)
+    # float64 norms in np.einsum's order: in fact bit for bit
+    assert r.centroids.tobytes() == g["centroids"].tobytes()
+    assert np.asarray(r.objectives).tobytes() == g["objectives"].tobytes()
 
 
 @pytest.mark.parametrize("case", cases(LLOYD))
