@@ -41,7 +41,7 @@ class ExecutionPlan:
     give the oracle's codes; "tensor" = the tcgen05 kernel, "guarded" = the
     FFMA kernel, "exact" = strict fp32 chains, "auto" = tensor where the
     shape allows it, else guarded), ``batch_rows`` (rows per host<->device batch; None =
-    max(block_size, 65536)), ``streams`` (CUDA streams in that pipeline),
+    ~256 MB of rows), ``streams`` (CUDA streams in that pipeline),
     ``device`` (CUDA ordinal; None = current) and ``devices`` (several ordinals: host rows
     are split into contiguous ranges, one pipeline per GPU on its own PCIe link -- the
     single-process counterpart of the reference's worker threads)."""
@@ -81,8 +81,13 @@ class ExecutionPlan:
     def resolved_w(self) -> int:
         return self.w if self.w is not None else native_lane_width()
 
-    def resolved_batch_rows(self) -> int:
-        return self.batch_rows if self.batch_rows is not None else max(self.block_size, 1 << 16)
+    def resolved_batch_rows(self, row_bytes: int = 4 * 768) -> int:
+        """Rows per host<->device batch: ``batch_rows``, else ~256 MB of input rows (16K..1M
+        rows).  Not derived from block_size, whose reference meaning (rows per CPU work item)
+        would size the pinned ring."""
+        if self.batch_rows is not None:
+            return self.batch_rows
+        return int(min(1 << 20, max(1 << 14, (256 << 20) // max(1, row_bytes))))
 
 
 @dataclass(frozen=True)
@@ -202,8 +207,9 @@ def _tc_ok(X, xrs, cbset) -> bool:
     t = torch()
     if not _tc_shape_ok(cbset, X.dtype == t.uint8):
         return False
-    if X.dtype == t.uint8:
-        return True
+    if X.dtype == t.uint8:  # one subvector per sub-byte cp.async (encode_tc_ex checks the same)
+        sub = cbset.sub_dim
+        return X.data_ptr() % sub == 0 and xrs % sub == 0
     return X.data_ptr() % 16 == 0 and (xrs * 4) % 16 == 0
 
 
@@ -300,6 +306,16 @@ def encode_dataset_host(X: np.ndarray, codebooks, plan: ExecutionPlan | None = N
     cdt = np.uint8 if cbset.k <= 256 else np.uint16
     if out is None:
         out = np.empty((n, cbset.m), dtype=cdt)
+    elif (not isinstance(out, np.ndarray) or out.dtype != cdt or out.shape != (n, cbset.m)
+          or not out.flags.c_contiguous or not out.flags.writeable):
+        # the C pipeline writes n * m codes linearly through out's buffer
+        raise ConfigError(f"out must be a writeable C-contiguous ({n}, {cbset.m}) {np.dtype(cdt).name} array")
+    batch_rows = plan.resolved_batch_rows(d * (1 if in_u8 else 4))
+    nb = -(-n // min(batch_rows, max(n, 1)))
+    if batch_ms is not None and (not isinstance(batch_ms, np.ndarray) or batch_ms.dtype != np.float64
+                                 or batch_ms.ndim != 1 or not batch_ms.flags.c_contiguous
+                                 or not batch_ms.flags.writeable or batch_ms.shape[0] < nb):
+        raise ConfigError(f"batch_ms must be a writeable contiguous float64 array of at least {nb} entries")
     if n == 0:
         return out
     if d != cbset.d:
@@ -312,9 +328,6 @@ def encode_dataset_host(X: np.ndarray, codebooks, plan: ExecutionPlan | None = N
     rm, bs, guard, vid = _variant_args(cbset, plan, precomputed_bias, dev)
     t = torch()
     t.cuda.current_stream(dev).synchronize()  # codebook upload visible to the pipeline streams
-    nb = -(-n // plan.resolved_batch_rows())
-    if batch_ms is not None and batch_ms.shape[0] < nb:
-        raise ConfigError("batch_ms too small")
     img = None
     if plan.mode in ("auto", "tensor") and vid != N.VARIANT_REFERENCE and _tc_shape_ok(cbset, in_u8):
         img = cbset.tc_image(dev, nobias=not precomputed_bias and plan.variant is EncoderVariant.BLOCKED)
@@ -324,7 +337,7 @@ def encode_dataset_host(X: np.ndarray, codebooks, plan: ExecutionPlan | None = N
     t.cuda.current_stream(dev).synchronize()  # image preparation visible to the pipeline streams
     N.call("cspq_encode_host", X.ctypes.data_as(ctypes.c_void_p), N.IN_U8 if in_u8 else N.IN_F32, n, d,
            ptr(rm), ptr(bs), ptr(guard), ptr(img), cbset.m, cbset.k, cbset.sub_dim,
-           out.ctypes.data_as(ctypes.c_void_p), vid, _MODES[plan.mode], plan.resolved_batch_rows(),
+           out.ctypes.data_as(ctypes.c_void_p), vid, _MODES[plan.mode], batch_rows,
            plan.streams, None if batch_ms is None else batch_ms.ctypes.data_as(ctypes.c_void_p),
            dev.index)
     return out

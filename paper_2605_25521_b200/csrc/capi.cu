@@ -4,6 +4,7 @@
 // pipeline (pinned ring, multi-stream overlap), and per-thread errors.
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -285,19 +286,29 @@ int cspq_encode_host(const void *X_host, int32_t in_dtype, int64_t n, int32_t d,
     const size_t esz = in_dtype == CSPQ_IN_U8 ? 1 : 4;
     const size_t cb = k <= 256 ? 1 : 2;
     const size_t xrow = (size_t)d * esz, crow = (size_t)m * cb;
+    // buffers for what this call can use (a 10-row call does not pin a 600 MB ring)
+    batch_rows = std::min<int64_t>(batch_rows, n);
     if ((rc = P.ensure(n_streams, batch_rows * xrow, batch_rows * crow))) return rc;
-    const bool pin_in = is_pinned(X_host), pin_out = is_pinned(codes_host);
-    const bool needs_guard = variant != CSPQ_VARIANT_REFERENCE && mode != CSPQ_MODE_EXACT;
-    if (needs_guard && !guard) {
-        if (P.guard_floats < (size_t)2 * m) {
-            if (P.guard) cudaFree(P.guard);
-            CSPQ_CUDA_TRY(cudaMalloc(reinterpret_cast<void **>(&P.guard), sizeof(float) * 2 * m));
-            P.guard_floats = 2 * m;
+    bool pin_in = is_pinned(X_host);
+    const bool pin_out = is_pinned(codes_host);
+    // pageable input: staged batch by batch through the pinned ring by a multi-threaded copy
+    // (30.8 GB/s of rows on the B200 box); CSPQ_HOST_REGISTER=1 page-locks the caller's array
+    // for the call instead (cudaHostRegister + DMA: 9.4 GB/s there -- registration dominates;
+    // scripts/probe_pageable.py)
+    bool registered = false;
+    if (!pin_in) {
+        const char *env = getenv("CSPQ_HOST_REGISTER");
+        const size_t in_bytes = (size_t)n * xrow;
+        const bool want = env && atoi(env) != 0;
+        void *hp = const_cast<void *>(X_host);
+        if (want && (cudaHostRegister(hp, in_bytes, cudaHostRegisterReadOnly) == cudaSuccess ||
+                     (cudaGetLastError(), cudaHostRegister(hp, in_bytes, cudaHostRegisterDefault) == cudaSuccess))) {
+            registered = pin_in = true;
+        } else {
+            cudaGetLastError();  // registration refused (e.g. already registered, or unsupported): stage instead
         }
-        if ((rc = encode_prepare(CB, B, m, k, sub, P.guard, P.st[0]))) return rc;
-        CSPQ_CUDA_TRY(cudaStreamSynchronize(P.st[0]));
-        guard = P.guard;
     }
+    const bool needs_guard = variant != CSPQ_VARIANT_REFERENCE && mode != CSPQ_MODE_EXACT;
     const int64_t nb = (n + batch_rows - 1) / batch_rows;
     std::vector<int64_t> slot_batch(n_streams, -1);
     auto retire = [&](int s) -> int {
@@ -314,32 +325,56 @@ int cspq_encode_host(const void *X_host, int32_t in_dtype, int64_t n, int32_t d,
         slot_batch[s] = -1;
         return CSPQ_OK;
     };
-    for (int64_t b = 0; b < nb; ++b) {
-        const int s = (int)(b % n_streams);
-        if ((rc = retire(s))) return rc;
-        const int64_t r0 = b * batch_rows, rows = std::min<int64_t>(batch_rows, n - r0);
-        const char *src = (const char *)X_host + r0 * xrow;
-        if (!pin_in) {
-            par_memcpy(P.hX[s], src, rows * xrow);
-            src = (const char *)P.hX[s];
+    auto run = [&]() -> int {
+        int rc2;
+        if (needs_guard && !guard) {
+            if (P.guard_floats < (size_t)2 * m) {
+                if (P.guard) cudaFree(P.guard);
+                P.guard = nullptr;
+                P.guard_floats = 0;
+                CSPQ_CUDA_TRY(cudaMalloc(reinterpret_cast<void **>(&P.guard), sizeof(float) * 2 * m));
+                P.guard_floats = 2 * m;
+            }
+            if ((rc2 = encode_prepare(CB, B, m, k, sub, P.guard, P.st[0]))) return rc2;
+            CSPQ_CUDA_TRY(cudaStreamSynchronize(P.st[0]));
+            guard = P.guard;
         }
-        cudaStream_t st = P.st[s];
-        CSPQ_CUDA_TRY(cudaEventRecord(P.ev0[s], st));
-        CSPQ_CUDA_TRY(cudaMemcpyAsync(P.dX[s], src, rows * xrow, cudaMemcpyHostToDevice, st));
-        if (tc_img && variant != CSPQ_VARIANT_REFERENCE)
-            rc = encode_tc(P.dX[s], in_dtype, rows, d, CB, B, guard, tc_img, m, k, sub,
-                           reinterpret_cast<uint8_t *>(P.dC[s]), m, nullptr, st);
-        else
-            rc = encode_device(P.dX[s], in_dtype, rows, d, d, CB, B, guard, m, k, sub, P.dC[s], m, variant, mode, st);
-        if (rc) return rc;
-        void *dst = pin_out ? (char *)codes_host + r0 * crow : P.hC[s];
-        CSPQ_CUDA_TRY(cudaMemcpyAsync(dst, P.dC[s], rows * crow, cudaMemcpyDeviceToHost, st));
-        CSPQ_CUDA_TRY(cudaEventRecord(P.ev1[s], st));
-        slot_batch[s] = b;
+        for (int64_t b = 0; b < nb; ++b) {
+            const int s = (int)(b % n_streams);
+            if ((rc2 = retire(s))) return rc2;
+            const int64_t r0 = b * batch_rows, rows = std::min<int64_t>(batch_rows, n - r0);
+            const char *src = (const char *)X_host + r0 * xrow;
+            if (!pin_in) {
+                par_memcpy(P.hX[s], src, rows * xrow);
+                src = (const char *)P.hX[s];
+            }
+            cudaStream_t st = P.st[s];
+            CSPQ_CUDA_TRY(cudaEventRecord(P.ev0[s], st));
+            CSPQ_CUDA_TRY(cudaMemcpyAsync(P.dX[s], src, rows * xrow, cudaMemcpyHostToDevice, st));
+            slot_batch[s] = b;  // from here on the stream may touch the caller's buffers
+            if (tc_img && variant != CSPQ_VARIANT_REFERENCE)
+                rc2 = encode_tc(P.dX[s], in_dtype, rows, d, CB, B, guard, tc_img, m, k, sub,
+                                reinterpret_cast<uint8_t *>(P.dC[s]), m, nullptr, st);
+            else
+                rc2 = encode_device(P.dX[s], in_dtype, rows, d, d, CB, B, guard, m, k, sub, P.dC[s], m, variant,
+                                    mode, st);
+            if (rc2) return rc2;
+            void *dst = pin_out ? (char *)codes_host + r0 * crow : P.hC[s];
+            CSPQ_CUDA_TRY(cudaMemcpyAsync(dst, P.dC[s], rows * crow, cudaMemcpyDeviceToHost, st));
+            CSPQ_CUDA_TRY(cudaEventRecord(P.ev1[s], st));
+        }
+        for (int s = 0; s < n_streams; ++s)
+            if ((rc2 = retire(s))) return rc2;
+        return CSPQ_OK;
+    };
+    rc = run();
+    if (rc != CSPQ_OK) {
+        // never return while copies into / out of the caller's buffers are still in flight
+        for (int s = 0; s < P.ns; ++s) cudaStreamSynchronize(P.st[s]);
+        cudaGetLastError();
     }
-    for (int s = 0; s < n_streams; ++s)
-        if ((rc = retire(s))) return rc;
-    return CSPQ_OK;
+    if (registered) cudaHostUnregister(const_cast<void *>(X_host));
+    return rc;
 }
 
 size_t cspq_crc32_workspace_bytes(int64_t n) { return crc32_workspace_bytes(n); }

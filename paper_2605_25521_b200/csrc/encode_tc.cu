@@ -760,6 +760,9 @@ int encode_tc_ex(const void *X, int in_dtype, int64_t n, int64_t xrs, int64_t xj
     const uint8_t *im = reinterpret_cast<const uint8_t *>(img);
     if (in_dtype == CSPQ_IN_U8) {
         const uint8_t *x = reinterpret_cast<const uint8_t *>(X);
+        // the x prefetch copies one subvector (sub bytes) with a sub-byte cp.async
+        CSPQ_REQUIRE(reinterpret_cast<uintptr_t>(x) % sub == 0 && xrs % sub == 0 && xjs % sub == 0, CSPQ_E_CONFIG,
+                     "tensor-core encode needs uint8 subvectors aligned to %d bytes", sub);
         return sub == 8 ? launch_tc<8, uint8_t>(x, n, m, xrs, xjs, CB, B, guard, im, codes, crs, cjs, flags, best, st)
                         : launch_tc<4, uint8_t>(x, n, m, xrs, xjs, CB, B, guard, im, codes, crs, cjs, flags, best, st);
     }

@@ -312,7 +312,7 @@ def encode_file(in_path, codebooks, out_path, plan=None, *, precomputed_bias: bo
     rc = N.load().cspq_encode_vecs_file(
         os.fsencode(str(in_path)), 0 if fmt == "fvecs" else 1, os.fsencode(str(out_path)), ptr(rm), ptr(bs),
         ptr(guard), ptr(img), cbset.m, cbset.k, cbset.sub_dim, vid, _MODES[plan.mode],
-        plan.resolved_batch_rows(), min(plan.streams, 8), dev.index, ctypes.byref(nrows), err)
+        plan.resolved_batch_rows(cbset.d * (4 if fmt == "fvecs" else 1)), min(plan.streams, 8), dev.index, ctypes.byref(nrows), err)
     if rc == N.CSPQ_E_FORMAT:
         kind, off, val = int(err[0]), int(err[1]), int(err[2])
         if kind == 4:

@@ -71,7 +71,10 @@ class TestPlanAndCodebooks:
         with pytest.raises(P.ConfigError):
             P.ExecutionPlan(mode="fast")
         assert P.ExecutionPlan().resolved_w() in (4, 8, 16)
-        assert P.ExecutionPlan(block_size=4096).resolved_batch_rows() == 65536
+        # ~256 MB of rows, not derived from block_size (a 1M-row block must not size a 9 GB ring)
+        assert P.ExecutionPlan(block_size=1_000_000).resolved_batch_rows(3072) == (256 << 20) // 3072
+        assert P.ExecutionPlan().resolved_batch_rows(128) == 1 << 20
+        assert P.ExecutionPlan().resolved_batch_rows(1 << 20) == 1 << 14
         assert P.ExecutionPlan(batch_rows=4096).resolved_batch_rows() == 4096
 
     def test_codebook_set(self):
