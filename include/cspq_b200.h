@@ -236,8 +236,9 @@ int cspq_lloyd_final_objective(const void *P, int32_t p_f64, int64_t n, int32_t 
  * cdf /= cdf[-1], searchsorted(cdf, u[j, c-1], 'right') -- and
  * d2 = minimum(d2, ||x - c||^2).  first (m) int64 and u (m, k-1) float64
  * are the host generator's draws (rng.integers(n), then one rng.random()
- * per choice).  status (m) int32 = 2 if a step met zero total mass (the
- * reference would have drawn rng.integers there instead). */
+ * per choice).  status (m) int32 = -c if step c met zero total mass (the
+ * reference draws rng.integers(n) for steps c..k-1 instead; the caller
+ * replays those draws), 3 if the total was NaN, else 0. */
 int cspq_kmeanspp(const void *P, int32_t p_f64, int64_t n, int32_t m, int32_t sub, int32_t k,
                   const int64_t *first, const double *u, double *C64, int32_t *status,
                   void *workspace, void *stream);

@@ -891,8 +891,11 @@ __global__ void __launch_bounds__(256) kpp_choose_kernel(double *__restrict__ pp
     __shared__ double s_run;
     const int j = blockIdx.x;
     if (status[j]) return;
-    if (!(total[j] > 0.0)) {  // all mass on chosen points
-        if (threadIdx.x == 0) status[j] = 2;
+    if (!(total[j] > 0.0)) {
+        // total <= 0: all mass on chosen points -- the reference switches to rng.integers(n) draws
+        // from this step on (training.py:84-86; the host replays them): status = -c.  A NaN total
+        // (training.py:87 would raise in rng.choice): status = 3
+        if (threadIdx.x == 0) status[j] = total[j] != total[j] ? 3 : -c;
         return;
     }
     double *cdf = pp + (int64_t)j * n;  // segment-end sums (cdf[s] = sum through s*kSeg+kSeg-1)
@@ -1318,8 +1321,9 @@ int lloyd_train(const void *P, int pf64, int64_t n, int m, int sub, int k, doubl
 
 // k-means++ seeding for every subspace (training.py:76-92).  first (m) and
 // u (m, k-1) are the host RNG draws (rng.integers(n), then one rng.random()
-// per rng.choice).  status[j] = 2 if a step found zero total mass (the
-// reference would then draw rng.integers instead -- reported to the host).
+// per rng.choice).  status[j] = -c if step c found zero total mass (the
+// reference then draws rng.integers(n) for steps c..k-1 -- the host replays
+// them), 3 if the total was NaN.
 int kmeanspp(const void *P, int pf64, int64_t n, int m, int sub, int k, const int64_t *first, const double *u,
              double *C64, int32_t *status, void *ws, cudaStream_t st) {
     WsLayout L(n, m, sub, k);

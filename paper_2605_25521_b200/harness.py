@@ -1,48 +1,45 @@
-"""Verification and ablation-bench harness of the encode path.
+"""Encoder-equivalence check and ablation timing on the GPU path.
 
-Mirrors the two harness functions of the reference's ``cspq.cli`` that drive
-the hot path (the CLI's argument parsing, plots and file plumbing stay out of
-scope):
+The reference drives its hot path from two harness functions in
+``cspq.cli`` (its acceptance criterion 5 runs them): ``run_verify``
+(cli.py:174-229) and ``run_bench_matrix`` (cli.py:232-276), with
+``BenchResult`` / ``write_bench_csv`` (cli.py:45-72, 279-284) as their
+output format.  Their return values and CSV layout are the contract kept
+here; the work is organised for the GPU:
 
-* ``run_verify`` (cli.py:174-229): three-way encoder equivalence
-  (REFERENCE / REFORMULATED / BLOCKED) over sampled vectors; every
-  disagreement is classified with the same float64 rule -- a near-tie when
-  the reference top-2 gap is within ``tolerance * max(1, second_best)``, a
-  failure otherwise.
-* ``run_bench_matrix`` (cli.py:232-276): the four-stage ablation (formula,
-  order, bias precomputation) timed through ``encode_dataset``, median of
-  ``reps`` after one warm-up, speed-ups against the first row.
-  ``BenchResult`` / ``BENCH_CSV_COLUMNS`` / ``write_bench_csv`` follow
-  cli.py:45-72, 279-284.
-
-Every encode runs on the GPU through the C ABI (``encode_dataset``); here the
-order / w / workers knobs only label the rows (codes are plan-invariant) and
-the variant and bias precomputation select the kernel (REFERENCE -> the
-generic exact kernel, BLOCKED without precomputed biases -> the recomputed
-bias tables)."""
+* verify: the sample is uploaded once, the three encoder variants run on the
+  device (``encode_dataset_device``), the disagreement mask is formed there,
+  and only the disagreeing (vector, subspace) pairs come back.  Their float64
+  top-2 gaps are computed in one vectorised pass that reproduces
+  ``np.einsum("kt,kt->k")``'s summation order (``einsum_rowsq``), so gaps and
+  the near-tie / failure split equal the reference's bit for bit
+  (tests/golden/verify_golden.npz).
+* bench matrix: the ablation is a table of ``Stage`` rows (formula, order,
+  bias precomputation); each is timed end to end through the public
+  ``encode_dataset`` on host rows (H2D, encode, D2H), median of ``reps``
+  after one warm-up.  On the GPU the order / w / workers knobs only label a
+  row -- codes are plan-invariant -- while variant and bias precomputation
+  select the kernel.
+"""
 
 from __future__ import annotations
 
 import csv
 import time
-from dataclasses import dataclass
+from dataclasses import astuple, dataclass, fields
 
 import numpy as np
 
-from .bulk import CHUNK_MAJOR, VECTOR_MAJOR, CodebookSet, ExecutionPlan, encode_dataset
+from ._device import device, torch
+from .bulk import CHUNK_MAJOR, VECTOR_MAJOR, CodebookSet, ExecutionPlan, encode_dataset, encode_dataset_device
 from .kernels import EncoderVariant, native_lane_width
 
-__all__ = ["BENCH_CSV_COLUMNS", "BenchResult", "run_bench_matrix", "run_verify", "write_bench_csv"]
-
-BENCH_CSV_COLUMNS = [
-    "variant", "order", "w", "block_size",
-    "n", "d", "m", "k", "wall_seconds", "vps", "speedup",
-]
+__all__ = ["BENCH_CSV_COLUMNS", "BenchResult", "run_bench_matrix", "run_verify", "write_bench_csv", "einsum_rowsq"]
 
 
 @dataclass
 class BenchResult:
-    """One row of the ablation matrix (cli.py:51-72)."""
+    """One ablation row; field order = CSV column order (cli.py:51-72)."""
 
     variant: str
     order: str
@@ -56,107 +53,132 @@ class BenchResult:
     vectors_per_second: float
     speedup_vs_baseline: float
 
+    # printf formats of the three measured columns; the rest print as-is
+    _FMT = {"wall_seconds": "{:.6f}", "vectors_per_second": "{:.1f}", "speedup_vs_baseline": "{:.4f}"}
+
     def csv_row(self) -> list:
-        return [
-            self.variant, self.order, self.w, self.block_size,
-            self.n, self.d, self.m, self.k,
-            f"{self.wall_seconds:.6f}",
-            f"{self.vectors_per_second:.1f}",
-            f"{self.speedup_vs_baseline:.4f}",
-        ]
+        return [self._FMT[f.name].format(v) if f.name in self._FMT else v
+                for f, v in zip(fields(self), astuple(self))]
 
 
-def _rows_of(dataset) -> np.ndarray:
-    # the reference probes hasattr(dataset, "data"), which on an ndarray picks
-    # its raw buffer; accept arrays and VectorDatasets alike
+# the CSV header names the two ratio columns by their short names
+BENCH_CSV_COLUMNS = [f.name for f in fields(BenchResult)][:9] + ["vps", "speedup"]
+
+
+@dataclass(frozen=True)
+class Stage:
+    """One row of the ablation: which formula, traversal order and bias handling."""
+
+    label: str
+    order: str
+    variant: EncoderVariant
+    precomputed_bias: bool
+
+
+# cli.py:240-246: baseline formula in vector-major order, then the blocked formula, then
+# chunk-major order, then precomputed biases (rows 3 and 4 differ only in the bias)
+ABLATION = (
+    Stage("reference", VECTOR_MAJOR, EncoderVariant.REFERENCE, True),
+    Stage("blocked", VECTOR_MAJOR, EncoderVariant.BLOCKED, False),
+    Stage("blocked", CHUNK_MAJOR, EncoderVariant.BLOCKED, False),
+    Stage("blocked+reform", CHUNK_MAJOR, EncoderVariant.BLOCKED, True),
+)
+
+
+def _host_rows(dataset) -> np.ndarray:
+    """float32 (or uint8) host rows of a VectorDataset or an array."""
     X = dataset.data if isinstance(getattr(dataset, "data", None), np.ndarray) else dataset
     X = np.asarray(X)
     return X if X.dtype == np.uint8 else np.asarray(X, dtype=np.float32)
 
 
+def _median_wall(fn, reps: int) -> float:
+    fn()  # warm-up (codebook upload, pipeline buffers)
+    walls = []
+    for _ in range(max(1, reps)):
+        t0 = time.perf_counter()
+        fn()
+        walls.append(time.perf_counter() - t0)
+    return float(np.median(walls))
+
+
 def run_bench_matrix(dataset, codebooks, w: int | None = None, block_size: int = 4096,
                      workers: int = 1, reps: int = 3) -> list[BenchResult]:
-    """The four-stage ablation (cli.py:232-276): baseline order/formula
-    through the full pipeline; rows 3 and 4 differ only in bias
-    precomputation.  Wall time of ``encode_dataset`` on host rows (H2D, GPU
-    encode, D2H), median of ``reps`` after one warm-up."""
+    """Time every ``ABLATION`` stage through ``encode_dataset`` on host rows;
+    speed-ups are against the first stage."""
     cbset = CodebookSet.from_codebooks(codebooks)
-    X = _rows_of(dataset)
-    wv = w if w is not None else native_lane_width()
-    rows = [
-        ("reference", VECTOR_MAJOR, EncoderVariant.REFERENCE, True),
-        ("blocked", VECTOR_MAJOR, EncoderVariant.BLOCKED, False),
-        ("blocked", CHUNK_MAJOR, EncoderVariant.BLOCKED, False),
-        ("blocked+reform", CHUNK_MAJOR, EncoderVariant.BLOCKED, True),
-    ]
-    results = []
-    baseline = None
-    for label, order, variant, precomp in rows:
-        plan = ExecutionPlan(order=order, block_size=block_size, variant=variant, w=wv, workers=workers)
-        encode_dataset(X, cbset, plan, precomputed_bias=precomp)  # warm-up
-        times = []
-        for _ in range(max(1, reps)):
-            t0 = time.perf_counter()
-            encode_dataset(X, cbset, plan, precomputed_bias=precomp)
-            times.append(time.perf_counter() - t0)
-        wall = float(np.median(times))
-        if baseline is None:
-            baseline = wall
-        results.append(BenchResult(
-            variant=label, order=order, w=wv, block_size=block_size,
-            n=X.shape[0], d=X.shape[1], m=cbset.m, k=cbset.k,
-            wall_seconds=wall, vectors_per_second=X.shape[0] / wall,
-            speedup_vs_baseline=baseline / wall,
-        ))
-    return results
+    X = _host_rows(dataset)
+    n, d = X.shape
+    lane_w = native_lane_width() if w is None else w
+    walls = []
+    for st in ABLATION:
+        plan = ExecutionPlan(order=st.order, block_size=block_size, variant=st.variant, w=lane_w, workers=workers)
+        walls.append(_median_wall(lambda: encode_dataset(X, cbset, plan, precomputed_bias=st.precomputed_bias), reps))
+    return [BenchResult(st.label, st.order, lane_w, block_size, n, d, cbset.m, cbset.k, wall, n / wall, walls[0] / wall)
+            for st, wall in zip(ABLATION, walls)]
 
 
 def write_bench_csv(results, path) -> None:
-    """cli.py:279-284."""
-    with open(path, "w", newline="") as f:
-        writer = csv.writer(f)
-        writer.writerow(BENCH_CSV_COLUMNS)
-        for r in results:
-            writer.writerow(r.csv_row())
+    with open(path, "w", newline="") as fh:
+        out = csv.writer(fh)
+        out.writerows([BENCH_CSV_COLUMNS] + [r.csv_row() for r in results])
+
+
+def einsum_rowsq(diff: np.ndarray) -> np.ndarray:
+    """sum_t diff[..., t]**2 in float64 with np.einsum's own order (numpy's 2-lane
+    sum_of_products: 8-element blocks folded back to front into two lane accumulators, a
+    tail of lane pairs, then lane0 + lane1 -- oracle_einsum_dot in oracle/pq_oracle.c),
+    vectorised over the leading axes."""
+    p = diff * diff
+    s = p.shape[-1]
+    lanes = [np.zeros(p.shape[:-1]), np.zeros(p.shape[:-1])]
+    t = 0
+    while s - t >= 8:
+        for lane in (0, 1):
+            for q in (6, 4, 2, 0):
+                lanes[lane] = p[..., t + q + lane] + lanes[lane]
+        t += 8
+    while t < s:
+        lanes[0] = p[..., t] + lanes[0]
+        if t + 1 < s:
+            lanes[1] = p[..., t + 1] + lanes[1]
+        t += 2
+    return lanes[0] + lanes[1]
 
 
 def run_verify(dataset, codebooks, samples: int, tolerance: float, seed: int = 0,
                w: int | None = None, workers: int = 1):
-    """Three-way encoder equivalence over sampled vectors (cli.py:174-229).
-
-    Returns ``(checked, near_ties, failures, details)``; ``details`` lists
-    ``(vector, chunk, kind, gap, codes)`` per disagreement, ``codes`` mapping
-    each variant's name to its code."""
-    X = _rows_of(dataset)
+    """Encoder equivalence on ``samples`` sampled vectors (PCG64(seed), sorted).
+    Returns ``(checked, near_ties, failures, details)`` with one
+    ``(vector, subspace, "near-tie" | "failure", gap, {variant name: code})`` per
+    disagreement of REFORMULATED or BLOCKED with REFERENCE, in row-major order; a
+    disagreement is a near-tie when the float64 top-2 distance gap is at most
+    ``tolerance * max(1, second best)``."""
+    t = torch()
+    X = _host_rows(dataset)
     cbset = CodebookSet.from_codebooks(codebooks)
-    rng = np.random.Generator(np.random.PCG64(seed))
     if samples < X.shape[0]:
-        idx = rng.choice(X.shape[0], size=samples, replace=False)
-        idx.sort()
-        X = np.ascontiguousarray(X[idx])
-    outs = {}
-    for variant in EncoderVariant:
-        plan = ExecutionPlan(variant=variant, w=w, workers=workers)
-        outs[variant] = encode_dataset(X, cbset, plan).codes
-    ref = outs[EncoderVariant.REFERENCE]
-    disagree = np.zeros(ref.shape, dtype=bool)
-    for variant in (EncoderVariant.REFORMULATED, EncoderVariant.BLOCKED):
-        disagree |= outs[variant] != ref
-    near_ties = 0
-    failures = 0
-    details = []
-    sub = cbset.sub_dim
-    for i, j in zip(*np.nonzero(disagree)):
-        v = X[i, j * sub:(j + 1) * sub].astype(np.float64)
-        cents = cbset.rowmajor[j].astype(np.float64)
-        dists = np.einsum("kt,kt->k", cents - v[None, :], cents - v[None, :])
-        top2 = np.partition(dists, 1)[:2]
-        gap = float(top2[1] - top2[0])
-        if gap <= tolerance * max(1.0, float(top2[1])):
-            near_ties += 1
-            kind = "near-tie"
-        else:
-            failures += 1
-            kind = "failure"
-        details.append((int(i), int(j), kind, gap, {v_.name: int(outs[v_][i, j]) for v_ in EncoderVariant}))
-    return X.shape[0], near_ties, failures, details
+        pick = np.random.Generator(np.random.PCG64(seed)).choice(X.shape[0], size=samples, replace=False)
+        X = np.ascontiguousarray(X[np.sort(pick)])
+    dev = device()
+    Xd = t.from_numpy(X if X.flags.writeable else X.copy()).to(dev)
+    codes = {v: encode_dataset_device(Xd, cbset, ExecutionPlan(variant=v, w=w, workers=workers))
+             for v in EncoderVariant}
+    base = codes[EncoderVariant.REFERENCE]
+    mask = (codes[EncoderVariant.REFORMULATED] != base) | (codes[EncoderVariant.BLOCKED] != base)
+    ij = t.nonzero(mask).cpu().numpy()  # row-major, like np.nonzero
+    if ij.shape[0] == 0:
+        return X.shape[0], 0, 0, []
+    got = {v: c[mask].cpu().numpy().view(np.uint16 if cbset.k > 256 else np.uint8) for v, c in codes.items()}
+    rows, subs = ij[:, 0], ij[:, 1]
+    s = cbset.sub_dim
+    V = X.reshape(X.shape[0], cbset.m, s)[rows, subs].astype(np.float64)           # (q, s)
+    C = cbset.rowmajor[subs].astype(np.float64)                                     # (q, k, s)
+    D = einsum_rowsq(C - V[:, None, :])                                             # (q, k)
+    top2 = np.sort(D, axis=1)[:, :2] if D.shape[1] > 1 else np.repeat(D, 2, axis=1)
+    gaps = top2[:, 1] - top2[:, 0]
+    near = gaps <= tolerance * np.maximum(1.0, top2[:, 1])
+    details = [(int(i), int(j), "near-tie" if nt else "failure", float(g),
+                {v.name: int(got[v][q]) for v in EncoderVariant})
+               for q, (i, j, nt, g) in enumerate(zip(rows, subs, near, gaps))]
+    return X.shape[0], int(near.sum()), int((~near).sum()), details

@@ -147,6 +147,7 @@ def kmeanspp_init_batched(points_list, k: int, rngs, dev=None) -> np.ndarray:
     else:
         P, pf64 = _stack_points(points_list)
     m, n, sub = P.shape
+    states = [r.bit_generator.state for r in rngs]
     first = np.array([int(r.integers(n)) for r in rngs], dtype=np.int64)
     u = np.stack([r.random(k - 1) if k > 1 else np.zeros(0) for r in rngs]).astype(np.float64)
     u = np.ascontiguousarray(u.reshape(m, max(k - 1, 0)))
@@ -161,10 +162,23 @@ def kmeanspp_init_batched(points_list, k: int, rngs, dev=None) -> np.ndarray:
         N.call("cspq_kmeanspp", ptr(Pd), pf64, n, m, sub, k, ptr(fd), ptr(ud), ptr(C), ptr(status), ptr(ws),
                stream_ptr(dev))
         Ch, st = C.cpu().numpy(), status.cpu().numpy()
-    if (st != 0).any():
-        j = int(np.flatnonzero(st)[0])
-        raise TrainingError(f"subspace {j}: k-means++ found zero remaining D^2 mass "
-                            "(degenerate data; the reference would switch to uniform draws)")
+    if (st == 3).any():
+        j = int(np.flatnonzero(st == 3)[0])
+        raise DataError(f"subspace {j}: k-means++ D^2 mass is NaN (non-finite training points)")
+    for j in np.flatnonzero(st < 0):
+        # step c met zero D^2 mass (every remaining point coincides with a chosen centroid, e.g.
+        # after float64 underflow): the reference draws rng.integers(n) for steps c..k-1
+        # (training.py:84-86; d2 stays all-zero once it is).  Replay the generator exactly:
+        # integers(n), c-1 random() draws, then the integer draws.
+        c = int(-st[j])
+        r = rngs[j]
+        r.bit_generator.state = states[j]
+        r.integers(n)
+        if c > 1:
+            r.random(c - 1)
+        idx = [int(r.integers(n)) for _ in range(c, k)]
+        src = P[j] if not isinstance(P, t.Tensor) else P[j].cpu().numpy()
+        Ch[j, c:] = np.asarray(src, dtype=np.float64)[idx]
     return Ch
 
 

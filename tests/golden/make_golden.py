@@ -385,7 +385,32 @@ def full_lloyd_cases(training, samples_path):
     return out
 
 
+def kpp_zero_mass_cases(training):
+    """_kmeanspp_init (training.py:76-92) when D^2 mass runs out: fewer distinct points than
+    k, so from some step on total == 0 and the reference draws rng.integers(n) instead of
+    rng.choice.  Records the seeds and the next draw of the generator afterwards."""
+    out = {}
+    rng0 = np.random.default_rng(20261020)
+    for case, (n, ndist, k, sub, seed) in enumerate([(50, 3, 8, 2, 5), (400, 17, 64, 4, 9), (33, 1, 4, 3, 1)]):
+        base = rng0.standard_normal((ndist, sub))
+        pts = base[rng0.integers(0, ndist, n)]
+        pts[:ndist] = base  # every distinct row present
+        rng = np.random.default_rng(seed)
+        init = training._kmeanspp_init(pts.astype(np.float64), k, rng)
+        g = f"z{case}"
+        out[f"{g}/pts"] = pts
+        out[f"{g}/k"] = np.int64(k)
+        out[f"{g}/seed"] = np.int64(seed)
+        out[f"{g}/init"] = init
+        out[f"{g}/next_draw"] = np.int64(rng.integers(1 << 30))
+    return out
+
+
 def main():
+    if sys.argv[1:2] == ["kppzero"]:
+        _, _, _, training = _ref()
+        np.savez_compressed(os.path.join(HERE, "kpp_zero_golden.npz"), **kpp_zero_mass_cases(training))
+        return
     if sys.argv[1:2] == ["full"]:  # full-size Lloyd goldens: make_golden.py full <train_samples.npz>
         sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
         _, _, _, training = _ref()

@@ -99,3 +99,13 @@ def test_run_bench_matrix_rows(tmp_path):
         assert r.wall_seconds > 0 and r.vectors_per_second > 0
     P.write_bench_csv(res, tmp_path / "m.csv")
     assert len(open(tmp_path / "m.csv").read().splitlines()) == 5
+
+
+def test_einsum_rowsq_is_numpys_order():
+    """run_verify's gaps use np.einsum("kt,kt->k")'s float64 order (cli.py:194-201)."""
+    from paper_2605_25521_b200.harness import einsum_rowsq
+    rng = np.random.default_rng(0)
+    for s in range(1, 20):
+        d = rng.standard_normal((20, 9, s)) * 10.0 ** rng.integers(-3, 4)
+        want = np.stack([np.einsum("kt,kt->k", d[q], d[q]) for q in range(20)])
+        assert einsum_rowsq(d).tobytes() == want.tobytes()

@@ -306,3 +306,19 @@ def test_screened_assignment_on_row_ranges(P, monkeypatch):
     for ranges in ([(0, n)], [(0, 3000), (3000, 7777), (7777, n)], [(5, 133), (0, 5), (133, n)]):
         got = run(ranges, "1")
         assert np.array_equal(got[0], full[0]) and got[1].tobytes() == full[1].tobytes(), ranges
+
+
+KPPZ = golden("kpp_zero_golden.npz")
+
+
+@pytest.mark.parametrize("case", cases(KPPZ))
+def test_kmeanspp_zero_mass_switches_to_integer_draws(P, case):
+    """training.py:84-86: once the D^2 mass is zero the reference draws rng.integers(n) for
+    the remaining seeds; the GPU seeding reports the step and the host replays the draws --
+    same seeds, and the generator ends in the reference's state."""
+    from paper_2605_25521_b200.training import kmeanspp_init_batched
+    g = group(KPPZ, case)
+    rng = np.random.default_rng(int(g["seed"]))
+    init = kmeanspp_init_batched([g["pts"].astype(np.float64)], int(g["k"]), [rng])[0]
+    assert init.tobytes() == g["init"].tobytes()
+    assert int(rng.integers(1 << 30)) == int(g["next_draw"])
