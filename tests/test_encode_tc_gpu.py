@@ -203,3 +203,25 @@ def test_every_centroid_index_decodes_tensor(P, oracle, sub):
     X2 = np.stack([dup[j, idx[:, j]] for j in range(m)], axis=1).reshape(k, m * sub)
     assert tc_codes(P, X2, cs2).tobytes() == oracle.encode(X2, cs2.rowmajor, cs2.biases,
                                                            oracle.VARIANT_REFORM).tobytes()
+
+
+@pytest.mark.parametrize("seed", [0, 7])
+def test_tensor_error_adversarial_search(seed):
+    """search adversarially for the worst tensor-core score error on
+    winners -- mixed-sign cancellation inside each K = 8 group, products spanning 2^-30..2^30,
+    tf32 hi/lo split extremes (maximal, zero and tie-boundary low parts), bias >> x.c and
+    bias << x.c, x ~ c -- with a hill-climb on the worst rows (scripts/tc_error_adversarial.py).
+    The guard flags runner-ups within 4E and needs |S_tc - s| <= 2E; the search must stay
+    below 0.6 E (3 seeds x 12 climbing rounds measured at most 0.37 E, profiles/)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "tc_adv", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts",
+                               "tc_error_adversarial.py"))
+    adv = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(adv)
+    rng = np.random.default_rng(seed)
+    for sub in (8, 4):
+        for name, (X, rm) in adv.families(rng, sub, n=8000).items():
+            worst = adv.climb(rng, X, rm, rounds=3)
+            assert worst < 0.6 * adv.E[sub], f"sub {sub} {name}: err/W {worst:.3e} = {worst / adv.E[sub]:.2f} E"
