@@ -121,24 +121,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         else if (clock64() - t0 > 20000000000ll) __trap();  // ~10 s: a lost arrival (not a time slice)
     }
 }
-// v2 wait: mbarrier.try_wait without a suspend-time hint (the hardware suspends the warp until the
-// phase completes or its own time limit) -- the hinted form compiles to NANOSLEEP.SYNCS, which
-// any mbarrier activity in the CTA wakes: with 16 epilogue warps that became a busy poll
-#ifndef CSPQ_TC2_SLEEP_NS
-#define CSPQ_TC2_SLEEP_NS 64
-#endif
-__device__ __forceinline__ void mbar_wait_hw(uint64_t *bar, uint32_t parity) {
-    uint32_t done = 0;
-    long long t0 = 0;
-    for (bool first = true;; first = false) {
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-        if (done) return;
-        if (first) t0 = clock64();
-        else if (clock64() - t0 > 20000000000ll) __trap();  // ~10 s: a lost arrival
-        __nanosleep(CSPQ_TC2_SLEEP_NS);  // a plain sleep: waiting warps leave the issue slots to the working ones
-    }
-}
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;
     asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
@@ -670,456 +652,6 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
     }
 }
 
-// ------------------------------------------------------------------ v2: teams of 8 epilogue warps
-// The v1 kernel above is bound by a round trip per TMEM accumulator: the MMA of item i + 2
-// waits until the scan of item i has read its last column, and one warp per lane quadrant
-// reads all 256 columns (4 x 64, three chunks of min trees before the last load).  v2 gives
-// every accumulator a TEAM of 8 warps -- two per TMEM lane quadrant, each reading one half
-// (128 columns = two tcgen05.ld x64): the buffer is handed back after one chunk of min trees
-// instead of three.  Two teams, one per TMEM buffer (team T owns items T, T + 2, ...):
-//   h1 warps (per row): A operand of the team's next item (x loaded one team item ahead into
-//     registers, Veltkamp split, ||x||), scan of columns 128..255 (16 block minima + 9 partial
-//     class minima), hand-off of those 25 minima + ||x|| to its h0 partner through shared memory
-//     (named barrier per (team, quadrant), double-buffered by item parity);
-//   h0 warps: scan of columns 0..127, combine, band-indicator selection, exact warp fix-up (or
-//     mark mode), code store.
-// Items are (row group of gs tiles, subspace) pairs x gs tiles, gs in {2, 4, 8}; the last row
-// group is padded with empty tiles (rows >= n are never stored), so an item index maps to its
-// pair and tile with shifts.
-constexpr int kTeams = 2;
-// warpgroup 0: MMA warp, loader warp, 2 idle warps (setmaxnreg: 32 registers); warpgroups 1-4: the
-// two teams (setmaxnreg: 112).  Five warps share each SM sub-partition's 16K registers, so without
-// the rebalancing every warp would get 96 (and the scans would spill)
-constexpr int kT2Threads = 128 + 256 * kTeams;
-constexpr int kT2RegsCtl = 32, kT2RegsEpi = 112;  // the CTA pool is the launch allocation (96 x 640)
-static_assert(kT2RegsCtl + 4 * kT2RegsEpi <= 5 * 96, "setmaxnreg.inc draws on the CTA pool = 96 registers x 640 threads at launch");
-constexpr int kPW = 44;  // floats per row record: 9 class minima of the producer (+3 pad), 16 + 16 block minima
-
-struct Tc2Hdr {
-    uint64_t b_full[2], b_empty[2];
-    uint64_t a_full[kTeams][2];
-    uint64_t t_full[kTeams], t_empty[kTeams];
-    uint32_t tmem_base;
-};
-
-template <int SUB>
-struct Tc2Smem {
-    using S = TcShape<SUB>;
-    static constexpr int kCFloats = kN * SUB + kN;
-    static constexpr size_t oB = 0;                                     // codebook image [2 pairs in flight]
-    static constexpr size_t oA = oB + 2 * (size_t)S::kBBytes;           // A operand [team][2]
-    static constexpr size_t oC = oA + 2 * kTeams * (size_t)S::kABytes;  // fp32 codebook + biases [2] (fix-up)
-    // row records [team][kTM][kPW]: one buffer suffices -- the producer of team item k + 2 writes
-    // only after that item's MMA, which needs every warp of the team (the selector of k included)
-    // to have loaded team item k + 1
-    static constexpr size_t oP = oC + 2 * (size_t)kCFloats * 4;
-    static constexpr size_t oG = oP + (size_t)kTeams * kTM * kPW * 4;  // guard constants (2 m floats)
-    static size_t total(int m) { return oG + ((size_t)2 * m * 4 + 15) / 16 * 16 + sizeof(Tc2Hdr) + 16; }
-};
-
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// a team's items li = T, T + 2, ... of the CTA's range; gs >= 2 so one step crosses at most one pair
-struct TeamIter {
-    int pair, p_end, g, j, t, m, gs;
-    __device__ TeamIter(int T, int p0, int p1, int m_, int gs_)
-        : pair(p0), p_end(p1), g(p0 / m_), j(p0 % m_), t(T), m(m_), gs(gs_) {}
-    __device__ bool valid() const { return pair < p_end; }
-    __device__ int64_t tile() const { return (int64_t)g * gs + t; }
-    __device__ void step() {
-        t += 2;
-        if (t >= gs) {
-            t -= gs;
-            ++pair;
-            if (++j == m) { j = 0; ++g; }
-        }
-    }
-};
-
-// one row's subvector, loaded straight into registers (an item ahead of its use)
-template <int SUB, typename TIn>
-struct XRow {
-    static constexpr int kWords = SUB * (int)sizeof(TIn) / 4;  // 32-bit words (u8 d_sub 4: 1)
-    uint32_t w[kWords];
-    __device__ void load(const TIn *src, bool ok) {
-        if constexpr (kWords >= 4) {
-#pragma unroll
-            for (int i = 0; i < kWords / 4; ++i) {
-                const uint4 v = ok ? __ldg(reinterpret_cast<const uint4 *>(src) + i) : make_uint4(0, 0, 0, 0);
-                w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
-            }
-        } else if constexpr (kWords == 2) {
-            const uint2 v = ok ? __ldg(reinterpret_cast<const uint2 *>(src)) : make_uint2(0, 0);
-            w[0] = v.x; w[1] = v.y;
-        } else {
-            w[0] = ok ? __ldg(reinterpret_cast<const uint32_t *>(src)) : 0u;
-        }
-    }
-    __device__ void to_float(float (&x)[SUB]) const {
-        if constexpr (sizeof(TIn) == 4) {
-#pragma unroll
-            for (int t = 0; t < SUB; ++t) x[t] = __uint_as_float(w[t]);
-        } else {
-#pragma unroll
-            for (int t = 0; t < SUB; ++t) x[t] = (float)((w[t >> 2] >> (8 * (t & 3))) & 255u);
-        }
-    }
-};
-
-template <int SUB, typename TIn, bool kMark, bool kBest>
-__global__ void __launch_bounds__(kT2Threads, 1)
-encode_tc2_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_t xjs, const float *__restrict__ CB,
-                  const float *__restrict__ Bv, const float *__restrict__ guard, const uint8_t *__restrict__ img,
-                  uint8_t *__restrict__ codes, int64_t cs, int64_t cjs, uint8_t *__restrict__ flags,
-                  float *__restrict__ best_out, int gs, int sched) {
-    // sched: always 0 at run time; tested between the two column chunks of a scan so that ptxas
-    // cannot hoist the second tcgen05.ld above the first chunk's min trees (128 live registers)
-    using S = TcShape<SUB>;
-    using L = Tc2Smem<SUB>;
-#ifdef CSPQ_TC_STAMPS
-    // (debug build, scripts/stamp_tc.py) sched bit 4: CTA 0 writes clock64 stamps per item into best_out
-    long long *stamp = (sched & 16) && blockIdx.x == 0 ? reinterpret_cast<long long *>(best_out) : nullptr;
-    if (sched & 16) best_out = nullptr;
-    sched &= 1;
-#else
-    constexpr long long *stamp = nullptr;
-#endif
-    constexpr uint32_t kStampItems = 2048;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *sB = smem_raw + L::oB;
-    unsigned char *sA = smem_raw + L::oA;
-    float *sC = reinterpret_cast<float *>(smem_raw + L::oC);
-    float *sP = reinterpret_cast<float *>(smem_raw + L::oP);
-    float *sGuard = reinterpret_cast<float *>(smem_raw + L::oG);
-    Tc2Hdr *H = reinterpret_cast<Tc2Hdr *>(smem_raw + L::oG + ((size_t)2 * m * 4 + 15) / 16 * 16);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // the CTA's contiguous range [p_begin, p_end) of (row group, subspace) pairs -- recomputed
-    // inside each role (values live across setmaxnreg.dec would be spilled)
-#define CSPQ_TC2_RANGE                                                                                  \
-    const int64_t npairs = ((((n + kTM - 1) / kTM) + gs - 1) / gs) * m;                                   \
-    const int p_begin = (int)(npairs * blockIdx.x / gridDim.x), p_end = (int)(npairs * (blockIdx.x + 1) / gridDim.x)
-
-    for (int i = threadIdx.x; i < 2 * m; i += kT2Threads) sGuard[i] = guard[i];
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&H->b_full[i], 1);
-            mbar_init(&H->b_empty[i], 1 + 256 * kTeams);  // MMA commit + every epilogue thread (fix-up reads sC)
-        }
-        for (int T = 0; T < kTeams; ++T) {
-            mbar_init(&H->a_full[T][0], 128);
-            mbar_init(&H->a_full[T][1], 128);
-            mbar_init(&H->t_full[T], 1);
-            mbar_init(&H->t_empty[T], 8);  // one elected lane per warp of the team
-        }
-        fence_mbar_init();
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&H->tmem_base)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = H->tmem_base;
-
-    if (warp < 4) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kT2RegsCtl));
-        CSPQ_TC2_RANGE;
-        if (warp == 0) {
-        // ---------------- MMA issuer: items in order, team T = item & 1 -> TMEM columns 256 T ----------------
-        uint32_t li = 0;
-        for (int p = p_begin; p < p_end; ++p) {
-            const uint32_t jt = (uint32_t)(p - p_begin), jb = jt & 1;
-            const uint32_t b0 = smem_u32(sB + jb * S::kBBytes);
-            mbar_wait_hw(&H->b_full[jb], (jt >> 1) & 1);
-            for (int t = 0; t < gs; ++t, ++li) {
-                const uint32_t T = li & 1, k = li >> 1;  // team, team item
-                const uint32_t a0 = smem_u32(sA + (T * 2 + (k & 1)) * S::kABytes);
-                uint64_t da[S::kSteps], db[S::kSteps];
-#pragma unroll
-                for (int s = 0; s < S::kSteps; ++s) {
-                    da[s] = make_desc(a0 + 2 * s * 128, 128, S::kRowGroupBytes);
-                    db[s] = make_desc(b0 + 2 * s * 128, 128, S::kRowGroupBytes);
-                }
-                mbar_wait_hw(&H->a_full[T][k & 1], (k >> 1) & 1);
-                if (stamp && lane == 0 && li < kStampItems) stamp[li * 8 + 0] = clock64();
-                if (k >= 1) mbar_wait_hw(&H->t_empty[T], (k - 1) & 1);  // team item k - 1 drained
-                if (stamp && lane == 0 && li < kStampItems) stamp[li * 8 + 1] = clock64();
-                tc_fence_after();
-                if (elect_one()) {
-#pragma unroll
-                    for (int s = 0; s < S::kSteps; ++s) mma_tf32(tmem + T * kN, da[s], db[s], s > 0);
-                    mma_commit(&H->t_full[T]);  // also frees A stage (T, k & 1)
-                }
-                __syncwarp();
-                if (stamp && lane == 0 && li < kStampItems) stamp[li * 8 + 2] = clock64();
-            }
-            if (elect_one()) mma_commit(&H->b_empty[jb]);
-            __syncwarp();
-        }
-        // teardown (the roles never meet again after setmaxnreg): wait for every epilogue warp
-        asm volatile("bar.sync 15, %0;" ::"n"(32 + 256 * kTeams) : "memory");
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-        } else if (warp == 1) {
-        // ---------------- codebook loader (as v1) ----------------
-        if (lane == 0) {
-            uint32_t jt = 0;
-            for (int p = p_begin; p < p_end; ++p, ++jt) {
-                const int j = p % m;
-                const int jb = jt & 1;
-                mbar_wait_hw(&H->b_empty[jb], ((jt >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&H->b_full[jb], S::kBBytes + L::kCFloats * 4);
-                bulk_g2s(sB + jb * S::kBBytes, img + (int64_t)j * S::kBBytes, S::kBBytes, &H->b_full[jb]);
-                float *cdst = sC + jb * L::kCFloats;
-                bulk_g2s(cdst, CB + (int64_t)j * kN * SUB, kN * SUB * 4, &H->b_full[jb]);
-                bulk_g2s(cdst + kN * SUB, Bv + (int64_t)j * kN, kN * 4, &H->b_full[jb]);
-            }
-        }
-        }
-    } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kT2RegsEpi));
-        CSPQ_TC2_RANGE;
-        const int ew = warp - 4;
-        const int T = ew >> 3;        // team
-        const int h = (ew >> 2) & 1;  // column half
-        const int q = warp & 3;        // TMEM lane quadrant (tcgen05.ld: warp w reads lanes 32 (w % 4) ..)
-        const int r = 32 * q + lane;   // tile row
-        const int bar_id = 1 + T * 4 + q;
-        const uint32_t tbase = tmem + ((uint32_t)(32 * q) << 16) + T * kN + h * 128;
-        constexpr float kE = tc_error_constant(SUB);
-        static_assert(S::kSteps == (SUB == 8 ? 4 : 2), "tc_error_constant counts K = 8 MMA steps");
-
-        // scan of this warp's 128 columns: 16 block minima (blocks of 7 and 9 per 16 columns; 8 per
-        // chunk go straight to shared memory at bmdst) and the 9 class minima over them; the TMEM
-        // buffer is handed back after the second load
-        auto scan = [&](uint32_t k, float (&cls)[kNCls], float *bmdst) {
-#pragma unroll
-            for (int c = 0; c < kNCls; ++c) cls[c] = pos_inf_f();
-            mbar_wait_hw(&H->t_full[T], k & 1);
-            const uint32_t sli = 2 * k + T;  // item index (stamps)
-            if (stamp && q == 0 && lane == 0 && sli < kStampItems) stamp[sli * 8 + 3 + 4 * h] = clock64();
-            tc_fence_after();
-#pragma unroll
-            for (int ch = 0; ch < 2; ++ch) {
-                uint32_t v[64];
-                tmem_ld64(tbase + ch * 64, v);
-                if (ch == 1) {  // every column of this warp is in registers: hand the buffer back
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&H->t_empty[T]);
-                    if (stamp && h == 0 && q == 0 && lane == 0 && sli < kStampItems) stamp[sli * 8 + 4] = clock64();
-                }
-#define SV(i) __uint_as_float(v[(i)])
-                if (sched) {
-                    cls[ch] = __fadd_rn(SV(0), SV(63));
-                    continue;
-                }
-                float bmc[8];
-#pragma unroll
-                for (int bp = 0; bp < 4; ++bp) {
-                    const int o = 16 * bp;
-#pragma unroll
-                    for (int c = 0; c < 7; ++c) cls[c] = fmin3(cls[c], SV(o + c), SV(o + 7 + c));
-                    if (bp & 1) {
-                        cls[7] = fmin3(cls[7], SV(o - 2), SV(o + 14));
-                        cls[8] = fmin3(cls[8], SV(o - 1), SV(o + 15));
-                    }
-                    bmc[2 * bp] = fmin3(fmin3(SV(o), SV(o + 1), SV(o + 2)), fmin3(SV(o + 3), SV(o + 4), SV(o + 5)), SV(o + 6));
-                    bmc[2 * bp + 1] = fmin3(fmin3(SV(o + 7), SV(o + 8), SV(o + 9)), fmin3(SV(o + 10), SV(o + 11), SV(o + 12)),
-                                            fmin3(SV(o + 13), SV(o + 14), SV(o + 15)));
-                }
-                reinterpret_cast<float4 *>(bmdst + 8 * ch)[0] = make_float4(bmc[0], bmc[1], bmc[2], bmc[3]);
-                reinterpret_cast<float4 *>(bmdst + 8 * ch)[1] = make_float4(bmc[4], bmc[5], bmc[6], bmc[7]);
-#undef SV
-            }
-        };
-
-        // Roles alternate inside each (team, quadrant) warp pair: for team item k the warp with
-        // h == k & 1 is the SELECTOR (scan of its half, then combine + band-indicator selection,
-        // fix-up, codes) and the other one the PRODUCER (A operand of team item k + 1 -- which it
-        // will select next -- then scan of its half and hand-off of its 9 class minima).  Both
-        // warps write their 16 block minima to the row's shared record; every warp thus does
-        // one selection and one A conversion per two team items.
-        float *rec = sP + ((size_t)T * kTM + r) * kPW;  // [9 class minima | 3 pad | 16 blocks h0 | 16 blocks h1]
-        unsigned char *arow = sA + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16;
-        // A row of team item k from the row's x (registers), Veltkamp split on the FMA pipe:
-        // xh = x rounded to 11 significant bits (exactly tf32), xl = x - xh exactly (the MMA
-        // reads xl truncated to tf32); returns ||x|| rounded up
-        auto convert = [&](const XRow<SUB, TIn> &xr, uint32_t k) -> float {
-            float x[SUB];
-            xr.to_float(x);
-            float xh[SUB], xl[SUB], ss = 0.f;
-#pragma unroll
-            for (int tt = 0; tt < SUB; ++tt) {
-                if constexpr (sizeof(TIn) == 1) {
-                    xh[tt] = x[tt];
-                    xl[tt] = 0.f;
-                } else {
-                    const float c = __fmul_rn(x[tt], 8193.0f);
-                    xh[tt] = __fsub_rn(c, __fsub_rn(c, x[tt]));
-                    xl[tt] = __fsub_rn(x[tt], xh[tt]);
-                }
-                ss = __fmaf_rn(x[tt], x[tt], ss);
-            }
-            unsigned char *rowp = arow + (T * 2 + (k & 1)) * S::kABytes;
-            auto st = [&](int c, float a0, float a1, float a2, float a3) {
-                *reinterpret_cast<float4 *>(rowp + c * 128) = make_float4(a0, a1, a2, a3);
-            };
-            if constexpr (SUB == 8) {
-                st(0, xh[0], xh[1], xh[2], xh[3]); st(1, xh[4], xh[5], xh[6], xh[7]);
-                st(2, xh[0], xh[1], xh[2], xh[3]); st(3, xh[4], xh[5], xh[6], xh[7]);
-                st(4, xl[0], xl[1], xl[2], xl[3]); st(5, xl[4], xl[5], xl[6], xl[7]);
-                st(6, 1.f, 1.f, 0.f, 0.f); st(7, 0.f, 0.f, 0.f, 0.f);
-            } else {
-                st(0, xh[0], xh[1], xh[2], xh[3]); st(1, xh[0], xh[1], xh[2], xh[3]);
-                st(2, xl[0], xl[1], xl[2], xl[3]); st(3, 1.f, 1.f, 0.f, 0.f);
-            }
-            fence_proxy_async();
-            mbar_arrive(&H->a_full[T][k & 1]);
-            return __fsqrt_ru(ss) * 1.000001f;
-        };
-        auto xsrc = [&](const TeamIter &it, bool &ok) -> const TIn * {
-            const int64_t row = it.tile() * kTM + r;
-            ok = it.valid() && row < n;
-            return X + (ok ? row * xs + (int64_t)it.j * xjs : 0);
-        };
-        // b_empty[p & 1] phase p >> 1 belongs to pair p; a warp that walks past a pair early first
-        // waits for pair p - 2's phase before arriving (as v1)
-        auto release_pair = [&](uint32_t p) {
-            mbar_wait_hw(&H->b_empty[p & 1], ((p >> 1) & 1) ^ 1);
-            mbar_arrive(&H->b_empty[p & 1]);
-        };
-
-        TeamIter cur(T, p_begin, p_end, m, gs);
-        TeamIter pf = cur;  // the next team item this warp converts (parity h), x in flight
-        XRow<SUB, TIn> xr;
-        float norm = 0.f;   // ||x|| of the row in the team item this warp selects next
-        bool ok;
-        if (h == 0) {  // team item 0: converted up front by its selector
-            xr.load(xsrc(pf, ok), ok);
-            if (pf.valid()) norm = convert(xr, 0);
-            pf.step();
-        }
-        pf.step();  // (h == 0: item 2; h == 1: item 1)
-        xr.load(xsrc(pf, ok), ok);
-        uint32_t rel = 0;
-        for (uint32_t k = 0; cur.valid(); ++k, cur.step()) {
-            const uint32_t jt = (uint32_t)(cur.pair - p_begin);
-            for (; rel < jt; ++rel) release_pair(rel);
-            const bool sel = (k & 1) == (uint32_t)h;
-            const uint32_t sli = 2 * k + T;  // item index (stamps)
-            if (!sel) {
-                // producer: A of team item k + 1 (this warp selects it), then the next x load
-                if (pf.valid()) norm = convert(xr, k + 1);
-                pf.step();
-                pf.step();
-                xr.load(xsrc(pf, ok), ok);
-            }
-            float cls[kNCls];
-            scan(k, cls, rec + 12 + 16 * h);
-            if (!sel) {
-                reinterpret_cast<float4 *>(rec)[0] = make_float4(cls[0], cls[1], cls[2], cls[3]);
-                reinterpret_cast<float4 *>(rec)[1] = make_float4(cls[4], cls[5], cls[6], cls[7]);
-                rec[8] = cls[8];
-                named_bar_sync(bar_id, 64);
-                continue;
-            }
-            named_bar_sync(bar_id, 64);
-            if (stamp && q == 0 && lane == 0 && sli < kStampItems) stamp[sli * 8 + 5] = clock64();
-            const int j = cur.j;
-            {
-                const float4 c0 = reinterpret_cast<const float4 *>(rec)[0];
-                const float4 c1 = reinterpret_cast<const float4 *>(rec)[1];
-                cls[0] = fminf(cls[0], c0.x); cls[1] = fminf(cls[1], c0.y); cls[2] = fminf(cls[2], c0.z);
-                cls[3] = fminf(cls[3], c0.w); cls[4] = fminf(cls[4], c1.x); cls[5] = fminf(cls[5], c1.y);
-                cls[6] = fminf(cls[6], c1.z); cls[7] = fminf(cls[7], c1.w); cls[8] = fminf(cls[8], rec[8]);
-            }
-            // band-indicator selection (v1): exactly one class minimum and one block minimum in
-            // the band => decided, and their indicator-weighted indices give class and block
-            const float m1 = fmin3(fmin3(cls[0], cls[1], cls[2]), fmin3(cls[3], cls[4], cls[5]), fmin3(cls[6], cls[7], cls[8]));
-            const float W = sGuard[2 * j] + norm * sGuard[2 * j + 1];
-            float kinv;
-            asm("rcp.approx.f32 %0, %1;" : "=f"(kinv) : "f"(4.0f * kE * W));  // inf for W = 0: flag
-            float qcf = 0.f, ncf = 0.f, wbf = 0.f, nbf = 0.f;
-#pragma unroll
-            for (int c = 0; c < kNCls; ++c) {
-                const float ind = __saturatef(__fmaf_rn(__fsub_rn(cls[c], m1), -kinv, 1.0f));
-                qcf = __fmaf_rn(ind, (float)(c + 8), qcf);
-                ncf = __fadd_rn(ncf, ind);
-            }
-#pragma unroll
-            for (int b4 = 0; b4 < 8; ++b4) {
-                const float4 t4 = reinterpret_cast<const float4 *>(rec + 12)[b4];
-                const float u[4] = {t4.x, t4.y, t4.z, t4.w};
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float ind = __saturatef(__fmaf_rn(__fsub_rn(u[i], m1), -kinv, 1.0f));
-                    wbf = __fmaf_rn(ind, (float)(4 * b4 + i + 32), wbf);
-                    nbf = __fadd_rn(nbf, ind);
-                }
-            }
-            const int64_t row = cur.tile() * kTM + r;
-            const int sb = __float2int_rz(wbf) - 32;
-            int code = 8 * sb - (sb & 1) + (__float2int_rz(qcf) - 8);
-            const bool flag = (row < n) && !(ncf == 1.0f && nbf == 1.0f);
-            if constexpr (kMark) {
-                if (row < n) flags[row * cs + j * cjs] = flag ? 1 : 0;
-                const unsigned fm = __ballot_sync(0xffffffffu, flag);
-                if (lane == 0 && fm) atomicAdd(&g_tc_flagged, (unsigned long long)__popc(fm));
-            }
-            unsigned mask = kMark ? 0u : __ballot_sync(0xffffffffu, flag);
-            if (mask) {
-                // exact warp-cooperative re-encode (x re-read from global; sC of this pair)
-                mbar_wait_hw(&H->b_full[jt & 1], (jt >> 1) & 1);
-                const float *cbs = sC + (jt & 1) * L::kCFloats;
-                if (lane == 0) atomicAdd(&g_tc_flagged, (unsigned long long)__popc(mask));
-                while (mask) {
-                    const int src = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    const int64_t srow = cur.tile() * kTM + 32 * q + src;
-                    const TIn *xp = X + srow * xs + (int64_t)j * xjs;
-                    float xv[SUB];
-#pragma unroll
-                    for (int tt = 0; tt < SUB; ++tt) xv[tt] = (float)xp[tt];
-                    float best = pos_inf_f();
-                    int bl = kN;
-#pragma unroll 2
-                    for (int l = lane; l < kN; l += 32) {
-                        float cv[SUB];
-#pragma unroll
-                        for (int tt = 0; tt < SUB; ++tt) cv[tt] = cbs[l * SUB + tt];
-                        const float sc = exact_score<SUB>(xv, cv, cbs[kN * SUB + l]);
-                        if (sc < best) { best = sc; bl = l; }
-                    }
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) {
-                        const float ob2 = __shfl_xor_sync(0xffffffffu, best, off);
-                        const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
-                        if (ob2 < best || (ob2 == best && ol < bl)) { best = ob2; bl = ol; }
-                    }
-                    if (lane == src) code = (best < pos_inf_f()) ? bl : 0;
-                }
-            }
-            if (row < n) {
-                codes[row * cs + j * cjs] = (uint8_t)code;
-                if constexpr (kBest) {
-                    if (best_out) best_out[row * m + j] = m1;
-                }
-            }
-            if (stamp && q == 0 && lane == 0 && sli < kStampItems) stamp[sli * 8 + 6] = clock64();
-        }
-        for (; rel < (uint32_t)(p_end - p_begin); ++rel) release_pair(rel);
-        tc_fence_before();
-        asm volatile("bar.arrive 15, %0;" ::"n"(32 + 256 * kTeams) : "memory");  // TMEM no longer read
-    }
-#undef CSPQ_TC2_RANGE
-}
-
-
 // Codebook image: per subspace, 256 rows (centroids) x K tf32 in the K-major
 // no-swizzle core-matrix layout the MMA reads.
 template <int SUB>
@@ -1153,55 +685,9 @@ __global__ void tc_image_kernel(const float *__restrict__ CB, const float *__res
         *reinterpret_cast<float4 *>(rowp + cch * 128) = make_float4(v[4 * cch], v[4 * cch + 1], v[4 * cch + 2], v[4 * cch + 3]);
 }
 
-// which tensor-core kernel: 1 = v1 (default), 2 = teams of 8 epilogue warps (CSPQ_TC_KERNEL=2; experiment, slower)
-int tc_kernel_version() {
-    static const int v = [] { const char *e = getenv("CSPQ_TC_KERNEL"); return e && atoi(e) == 2 ? 2 : 1; }();
-    return v;
-}
-
-template <int SUB, typename TIn>
-int launch_tc2(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const float *CB, const float *B, const float *guard,
-               const uint8_t *img, uint8_t *codes, int64_t cs, int64_t cjs, uint8_t *flags, float *best, cudaStream_t st) {
-    const size_t smem = Tc2Smem<SUB>::total(m);
-    CSPQ_REQUIRE(smem <= 227 * 1024, CSPQ_E_CONFIG, "too many subspaces (%d) for the tensor-core kernel", m);
-    auto kern = flags ? (best ? encode_tc2_kernel<SUB, TIn, true, true> : encode_tc2_kernel<SUB, TIn, true, false>)
-                      : (best ? encode_tc2_kernel<SUB, TIn, false, true> : encode_tc2_kernel<SUB, TIn, false, false>);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    static int sm_count[64] = {};
-    static std::atomic<uint32_t> smem_set[64][2][2] = {};
-    const int di = dev & 63;
-    if (!sm_count[di]) {
-        int v = 148;
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        sm_count[di] = v;
-    }
-    std::atomic<uint32_t> &once = smem_set[di][flags ? 1 : 0][best ? 1 : 0];
-    if (!once.load(std::memory_order_acquire)) {
-        CSPQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        once.store(1, std::memory_order_release);
-    }
-    const int64_t ntiles = (n + kTM - 1) / kTM;
-    // tiles per row group: a power of two >= 2 (teams alternate items; the last group is padded)
-    const int gs = ntiles >= kG ? kG : (ntiles > 2 ? 4 : 2);
-    const int64_t ngroups = (ntiles + gs - 1) / gs;
-    CSPQ_REQUIRE(ngroups * m < ((int64_t)1 << 31), CSPQ_E_CONFIG, "too many rows (%lld) for one launch", (long long)n);
-    const int grid = (int)std::min<int64_t>(sm_count[di], ngroups * m);
-#ifdef CSPQ_TC_STAMPS
-    const char *pe = getenv("CSPQ_TC_PROBE");
-    const int sched = pe ? (atoi(pe) & 16) : 0;
-#else
-    const int sched = 0;
-#endif
-    kern<<<grid, kT2Threads, smem, st>>>(X, n, m, xs, xjs, CB, B, guard, img, codes, cs, cjs, flags, best, gs, sched);
-    CSPQ_LAUNCH_CHECK();
-    return CSPQ_OK;
-}
-
 template <int SUB, typename TIn>
 int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const float *CB, const float *B, const float *guard,
               const uint8_t *img, uint8_t *codes, int64_t cs, int64_t cjs, uint8_t *flags, float *best, cudaStream_t st) {
-    if (tc_kernel_version() == 2) return launch_tc2<SUB, TIn>(X, n, m, xs, xjs, CB, B, guard, img, codes, cs, cjs, flags, best, st);
     const size_t smem = TcSmem<SUB, TIn>::total(m);
     CSPQ_REQUIRE(smem <= 227 * 1024, CSPQ_E_CONFIG, "too many subspaces (%d) for the tensor-core kernel", m);
     CSPQ_REQUIRE((n + kTM - 1) / kTM < ((int64_t)1 << 31), CSPQ_E_CONFIG, "too many rows (%lld) for one launch", (long long)n);
@@ -1297,10 +783,6 @@ int encode_tc(const void *X, int in_dtype, int64_t n, int64_t xrs, const float *
 float encode_tc_error_constant(int sub) { return tc_error_constant(sub); }
 
 int encode_tc_max_subspaces(int sub, int in_dtype) {
-    if (tc_kernel_version() == 2) {
-        auto fit2 = [](size_t fixed) { return (int)((227 * 1024 - fixed - sizeof(Tc2Hdr) - 16) / 8 / 4 * 4); };
-        return sub == 8 ? fit2(Tc2Smem<8>::oG) : sub == 4 ? fit2(Tc2Smem<4>::oG) : 0;
-    }
     auto fit = [](size_t fixed) { return (int)((227 * 1024 - fixed - sizeof(TcSmemHdr) - 16) / 8 / 4 * 4); };
     if (sub == 8) return in_dtype == CSPQ_IN_U8 ? fit(TcSmem<8, uint8_t>::oG) : fit(TcSmem<8, float>::oG);
     if (sub == 4) return in_dtype == CSPQ_IN_U8 ? fit(TcSmem<4, uint8_t>::oG) : fit(TcSmem<4, float>::oG);
