@@ -283,28 +283,13 @@ def run_reference(args, ws, rank):
 
 # ----------------------------------------------------------------------------------- B200 arm
 def count_launches(fn):
-    """Kernel launches of one call of ``fn`` seen by CUPTI (torch.profiler), split into this
-    repo's kernels and others (torch fills/copies)."""
-    try:
-        import torch
-        from torch.profiler import ProfilerActivity, profile
-        with profile(activities=[ProfilerActivity.CUDA], acc_events=True) as prof:
-            fn()
-            torch.cuda.synchronize()
-        ours = other = 0
-        for ev in prof.events():
-            if getattr(ev, "device_type", None) is None or str(ev.device_type) != "DeviceType.CUDA":
-                continue
-            name = ev.name or ""
-            if name.startswith("Memcpy") or name.startswith("Memset"):
-                continue
-            if "cspq" in name:
-                ours += 1
-            else:
-                other += 1
-        return ours, other
-    except Exception:
-        return None, None
+    """This library's kernel launches in one call of ``fn`` (cspq_launch_count: a host-side
+    counter bumped at every launch site of libcspq_b200.so)."""
+    from paper_2605_25521_b200 import _native as N
+    L = N.load()
+    L.cspq_launch_count(1)
+    fn()
+    return int(L.cspq_launch_count(1))
 
 
 def train_codebooks(cfg, args, ws, rank, dev, timed_train=False):
@@ -595,7 +580,7 @@ def run_config(cfg, args, ws, rank, local, dev, steps, warmup, cpu_seconds, head
     N.call("cspq_encode_stats", ctypes.byref(fl), 1)
     ms_per_step = total_ms / steps
     value = global_rows * steps / (total_ms / 1e3)
-    ours, other = count_launches(step)
+    launches_per_step = count_launches(step)
 
     # encode-kernel-only timing for c2 (its step also trains): the roofline is the encode kernel's
     enc_ms = ms_per_step
@@ -621,15 +606,13 @@ def run_config(cfg, args, ws, rank, local, dev, steps, warmup, cpu_seconds, head
                        "rows_per_gpu": rows, "parallelism": f"rows sharded x{ws} (codebooks broadcast)",
                        "mode": args.mode, "codebook_train_s": tinfo["train_s"],
                        "codebook_training": tinfo["mode"], "l2": l2_note},
-            "clocks": clk, "e2e": e2e, "gpu_launches": None if ours is None else ours * steps,
-            "gpu_launches_def": "this repo's kernels (names in namespace cspq) per step x steps, counted by CUPTI "
-                                "(torch.profiler) on one extra untimed step",
+            "clocks": clk, "e2e": e2e, "gpu_launches": launches_per_step * steps,
+            "gpu_launches_def": "libcspq_b200.so kernel launches per step (host-side launch counter, "
+                                "cspq_launch_count, on one extra untimed step) x steps",
             "roofline": roofline_record(cfg, args, rows, enc_ms, dev), "parity": parity,
             "flagged_per_subvector": fl.value / max(1, rows * cfg.m * (steps if cfg.name != "c2" else steps + warmup)),
             "step_ms": step_ms,
         }
-        if other:
-            rec["other_launches_per_step"] = other
         if cfg.name == "c2":
             rec["train"] = {"gpu_s": tinfo["train_s"], "subspaces": cfg.m, "iters": cfg.iters,
                             "sample_rows": cfg.n_train, "encode_ms": enc_ms,

@@ -90,6 +90,10 @@ int cspq_encode_set_tiling(int32_t tiling);
  * device.  reset != 0 zeroes the counter after reading. */
 int cspq_encode_stats(uint64_t *flagged, int32_t reset);
 
+/* Number of kernels this library has launched in the process (host-side count, one per launch
+ * site execution); reset != 0 returns the count and zeroes it.  bench.py's gpu_launches. */
+uint64_t cspq_launch_count(int32_t reset);
+
 /* Bias table of the precomputed_bias=False ablation (kernels.py:146-157):
  * B_out[j,l] = 0.5f * fl-chain(sum_t c_t*c_t) in float32, exactly as the
  * reference recomputes it per vector.  (m, k) float32 device buffer. */

@@ -36,6 +36,7 @@ _SIGS = {
     "cspq_abi_version": ([], _i32),
     "cspq_last_error": ([], ctypes.c_char_p),
     "cspq_encode_stats": ([_vp, _i32], _i32),
+    "cspq_launch_count": ([_i32], ctypes.c_uint64),
     "cspq_encode_set_tiling": ([_i32], _i32),
     "cspq_encode_tc_image_bytes": ([_i32, _i32, _i32], ctypes.c_size_t),
     "cspq_encode_tc_max_subspaces": ([_i32, _i32], _i32),

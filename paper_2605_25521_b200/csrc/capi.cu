@@ -3,6 +3,7 @@
 // reference's error classes, the end-to-end host->device->host encode
 // pipeline (pinned ring, multi-stream overlap), and per-thread errors.
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstring>
@@ -154,6 +155,9 @@ struct Pipeline {
 Pipeline g_pipes[64];
 }  // namespace
 
+std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 void set_error(const char *fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
@@ -171,6 +175,10 @@ int cspq_abi_version(void) { return CSPQ_ABI_VERSION; }
 const char *cspq_last_error(void) { return g_err; }
 
 int cspq_encode_set_tiling(int32_t tiling) { return encode_set_tiling(tiling); }
+
+uint64_t cspq_launch_count(int32_t reset) {
+    return reset ? g_launches.exchange(0, std::memory_order_relaxed) : g_launches.load(std::memory_order_relaxed);
+}
 
 int cspq_encode_stats(uint64_t *flagged, int32_t reset) {
     unsigned long long v = 0, w = 0;

@@ -11,6 +11,9 @@ namespace cspq {
 
 // per-thread last-error message (cspq_last_error)
 void set_error(const char *fmt, ...);
+// host-side count of this library's kernel launches (cspq_launch_count): every launch site is
+// followed by exactly one CSPQ_LAUNCH_CHECK
+void count_launch();
 
 #define CSPQ_CUDA_TRY(expr)                                                              \
     do {                                                                                 \
@@ -22,7 +25,11 @@ void set_error(const char *fmt, ...);
         }                                                                                \
     } while (0)
 
-#define CSPQ_LAUNCH_CHECK() CSPQ_CUDA_TRY(cudaGetLastError())
+#define CSPQ_LAUNCH_CHECK()              \
+    do {                                 \
+        ::cspq::count_launch();          \
+        CSPQ_CUDA_TRY(cudaGetLastError()); \
+    } while (0)
 
 #define CSPQ_REQUIRE(cond, code, ...)                                                    \
     do {                                                                                 \
