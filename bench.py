@@ -549,7 +549,7 @@ def run_config(cfg, args, ws, rank, local, dev, steps, warmup, cpu_seconds, head
             csteps = CudaSteps(Ssm, 0, cfg.n_train, cfg.m, cfg.sub, cfg.k, dev)
             train_step = lambda: lloyd_sharded(csteps, init_d, tcfg, reduce=args.reduce)
         else:
-            train_step = lambda: P.lloyd_iterate_batched(Ssm, init_np, tcfg)
+            train_step = lambda: P.lloyd_iterate_batched(Ssm, init_np, tcfg, return_assignments=False)
         if rank == 0 and "results" in tinfo:
             parity["train"] = train_parity(cfg, dev, tinfo["results"])
 
@@ -561,7 +561,7 @@ def run_config(cfg, args, ws, rank, local, dev, steps, warmup, cpu_seconds, head
 
         Ssm_h = P.pinned_empty(tuple(Ssm.shape), np.float32)
         Ssm_h[:] = Ssm.cpu().numpy()
-        train_host = lambda: cs_of(P.lloyd_iterate_batched(Ssm_h, init_np, tcfg))
+        train_host = lambda: cs_of(P.lloyd_iterate_batched(Ssm_h, init_np, tcfg, return_assignments=False))
     else:
         def step():
             P.encode_dataset_device(X, cs, plan, out=out)
@@ -619,7 +619,7 @@ def run_config(cfg, args, ws, rank, local, dev, steps, warmup, cpu_seconds, head
                             "train_ms_in_step": ms_per_step - enc_ms,
                             "encode_only_vec_s": global_rows / (enc_ms / 1e3),
                             "def": "value = N / (training of all subspaces (fp64, tol 0, incl. the final REFERENCE "
-                                   "pass and the host copy of KMeansResult) + encode of all rows), per step"}
+                                   "pass, centroids and objective traces copied to the host) + encode of all rows), per step"}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         gen = lambda r: C.generate(cfg, 0, r, dev).cpu().numpy()
         cpu = cpu_baseline_record(cfg, cs.rowmajor, cs.biases, gen, cpu_seconds)

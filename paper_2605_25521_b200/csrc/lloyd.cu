@@ -24,6 +24,7 @@
 //     subspace (state[j]) so every subspace runs exactly the iterations the
 //     reference's sequential loop would.
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -43,6 +44,7 @@ constexpr uint64_t kMagic = 0x43535051424C4C59ull;
 
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
+
 struct WsLayout {
     int64_t header, leaves, nodes, ntmp, nodeval, hist, cnt, start, perm, sq, resid, leafsum, cn;
     // train-loop state
@@ -51,6 +53,7 @@ struct WsLayout {
     int64_t p32, d2, pp;
     // tensor-core screened assignment: float32 codebooks, biases, guard, tcgen05 image, codes, flags
     int64_t tc_cb, tc_b, tc_guard, tc_img, tc_codes, tc_flags, tc_rmax;
+    int64_t redo;  // clusters whose sums need the sequential chain (sums_exact_kernel)
     int64_t total;
     int64_t nch, maxleaves;
     WsLayout(int64_t n, int m, int sub, int k) {
@@ -89,6 +92,7 @@ struct WsLayout {
         tc_codes = take((int64_t)m * n);
         tc_flags = take((int64_t)m * n);
         tc_rmax = take(4 * (int64_t)m);
+        redo = take((int64_t)m * k);
         total = o;
     }
     template <typename T>
@@ -101,6 +105,7 @@ struct WsHeader {
     int64_t nleaves;
     int64_t nlevels;     // heights 1 .. nlevels of the internal nodes
 };
+
 
 // ---------------------------------------------------------------- pairwise tree
 // Leaves of numpy's pairwise summation of a length-n range, in order
@@ -309,6 +314,9 @@ __device__ __forceinline__ double einsum_sum(G prod, int n) {
 }
 
 // ---------------------------------------------------------------- assignment
+#ifndef CSPQ_SETTLE_PPT
+#define CSPQ_SETTLE_PPT 2  // points per thread per step in tc_settle_kernel
+#endif
 #ifndef CSPQ_LLOYD_PPT
 #define CSPQ_LLOYD_PPT 4  // points per thread in assign_kernel (2x4, 4x2, 4x4, 2x8, 1x8 measured: 4x2 best)
 #endif
@@ -483,7 +491,7 @@ tc_settle_kernel(const float *__restrict__ P, int64_t n, int k, const double *__
     // loop bound is warp-uniform (a warp owns 64 consecutive points) so flagged points can be
     // scanned by the whole warp: lanes split the 256 centroids, then a shuffle reduction keeps the
     // sequential scan's winner (smallest d, first index; a NaN d never wins unless it is d_0)
-    constexpr int kPP = 2;
+    constexpr int kPP = CSPQ_SETTLE_PPT;
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kPP;
     for (int64_t w0 = b + ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * kPP; w0 < e; w0 += stride) {
@@ -664,14 +672,14 @@ template <int SUBC, typename TP>
 __global__ void sums_kernel(const TP *__restrict__ P, int64_t n, int m, int k, int sub_rt,
                             const int32_t *state, int64_t b, const int32_t *__restrict__ cnt,
                             const int32_t *__restrict__ start, const int32_t *__restrict__ perm,
-                            double *__restrict__ sums) {
+                            double *__restrict__ sums, const uint8_t *__restrict__ only) {
     const int sub = SUBC > 0 ? SUBC : sub_rt;
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= (int64_t)m * k * sub) return;
     const int t = (int)(g % sub);
     const int64_t jl = g / sub;
     const int j = (int)(jl / k);
-    if (!state[j]) return;
+    if (!state[j] || (only && !only[jl])) return;
     const int32_t c0 = start[jl], cc = cnt[jl];
     const int32_t *pp = perm + (int64_t)j * n + c0;
     const TP *Pj = P + ((int64_t)j * n + b) * sub + t;
@@ -697,6 +705,88 @@ __global__ void sums_kernel(const TP *__restrict__ P, int64_t n, int m, int k, i
     }
     for (; p < cc; ++p) s = __dadd_rn(s, (double)Pj[(int64_t)pp[p] * sub]);
     sums[g] = s;
+}
+
+// sums[j][l][:] for float32 points, one warp per (subspace, cluster).  np.add.at's result is the
+// sequential float64 chain over the cluster's points in ascending order; when that chain cannot
+// round, its value is the exact sum and any order gives it.  It cannot round when every member
+// value is a multiple of 2^L (L = the lowest set bit over the members' coordinates) and
+// count * max|v| <= 2^(L + 52): every partial sum -- of the chain or of any subset -- is then a
+// multiple of 2^L below 2^(L + 53), exactly representable.  The warp checks that while it sums
+// lane-strided partials (a parallel reduction); a cluster that fails the check (float32 data with
+// tiny values, NaN/inf) is marked in redo[] and summed again by sums_kernel's sequential chains.
+// Measured on the config samples: c2 and c4 never fail, c3 / c5 ~4 of 256 clusters per subspace.
+template <int SUBC>
+__global__ void __launch_bounds__(128)
+sums_exact_kernel(const float *__restrict__ P, int64_t n, int m, int k, const int32_t *state, int64_t b,
+                  const int32_t *__restrict__ cnt, const int32_t *__restrict__ start,
+                  const int32_t *__restrict__ perm, double *__restrict__ sums, uint8_t *__restrict__ redo) {
+    const int64_t jl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (jl >= (int64_t)m * k) return;
+    const int j = (int)(jl / k);
+    if (!state[j]) return;
+    const int32_t c0 = start[jl], cc = cnt[jl];
+    const int32_t *pp = perm + (int64_t)j * n + c0;
+    const float *Pj = P + ((int64_t)j * n + b) * SUBC;
+    double acc[SUBC];
+#pragma unroll
+    for (int t = 0; t < SUBC; ++t) acc[t] = 0.0;
+    int minlsb = 1 << 20;
+    uint32_t maxabs = 0;
+    // kU members per lane in flight (independent index and row loads): the gathers are
+    // latency-bound, not bandwidth-bound
+    constexpr int kU = 4;
+    for (int32_t p0 = lane; p0 < cc; p0 += 32 * kU) {
+        int32_t idx[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) idx[u] = p0 + 32 * u < cc ? __ldg(pp + p0 + 32 * u) : -1;
+        float x[kU][SUBC];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const float4 *xp = reinterpret_cast<const float4 *>(Pj + (int64_t)(idx[u] < 0 ? 0 : idx[u]) * SUBC);
+#pragma unroll
+            for (int q = 0; q < SUBC / 4; ++q) {
+                const float4 v = idx[u] < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(xp + q);
+                x[u][4 * q] = v.x; x[u][4 * q + 1] = v.y; x[u][4 * q + 2] = v.z; x[u][4 * q + 3] = v.w;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+#pragma unroll
+            for (int t = 0; t < SUBC; ++t) {
+                acc[t] = __dadd_rn(acc[t], (double)x[u][t]);
+                const uint32_t a = __float_as_uint(x[u][t]) & 0x7fffffffu;
+                maxabs = max(maxabs, a);  // non-negative float bits order like the values (inf / NaN largest)
+                if (a) {
+                    const int e = (int)(a >> 23);
+                    const uint32_t mant = e ? ((a & 0x7fffffu) | 0x800000u) : a;
+                    minlsb = min(minlsb, (e ? e - 150 : -149) + __ffs(mant) - 1);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+#pragma unroll
+        for (int t = 0; t < SUBC; ++t) acc[t] = __dadd_rn(acc[t], __shfl_xor_sync(0xffffffffu, acc[t], o));
+        minlsb = min(minlsb, __shfl_xor_sync(0xffffffffu, minlsb, o));
+        maxabs = max(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, o));
+    }
+    const double bound = (double)cc * (double)__uint_as_float(maxabs);  // >= sum |v| (inf / NaN: fails)
+    const bool exact = minlsb >= (1 << 20) || bound <= ldexp(1.0, minlsb + 52);
+    double *out = sums + jl * SUBC;
+    if (lane == 0) redo[jl] = 0;
+    if (exact) {
+        if (lane < SUBC) {
+            double v = acc[0];
+#pragma unroll
+            for (int t = 1; t < SUBC; ++t) v = lane == t ? acc[t] : v;
+            out[lane] = v;
+        }
+        return;
+    }
+    if (lane == 0) redo[jl] = 1;  // sums_kernel runs the sequential chain of this cluster
 }
 
 // ---------------------------------------------------------------- update / repair / stop
@@ -1027,7 +1117,7 @@ static int assign_tc(const float *P, int64_t n, int m, int sub, int k, const dou
                            flags + b, nullptr, st)))
         return rc;
     // ~8 CTAs per SM in total: each CTA stages its subspace's codebook once for many points
-    dim3 grid((unsigned)grid_for((e - b + 1) / 2, 256, std::max<int64_t>(1, 148 * 8 / m)), (unsigned)m);
+    dim3 grid((unsigned)grid_for((e - b + CSPQ_SETTLE_PPT - 1) / CSPQ_SETTLE_PPT, 256, std::max<int64_t>(1, 148 * 8 / m)), (unsigned)m);
     if (sub == 8) tc_settle_kernel<8><<<grid, 256, 0, st>>>(P, n, k, C64, cn, state, b, e, codes, flags, assign, sq);
     else tc_settle_kernel<4><<<grid, 256, 0, st>>>(P, n, k, C64, cn, state, b, e, codes, flags, assign, sq);
     CSPQ_LAUNCH_CHECK();
@@ -1227,10 +1317,21 @@ int lloyd_accumulate(const void *P, int pf64, int64_t n, int m, int sub, int k, 
     }
     const int64_t tot = (int64_t)m * k * sub;
     const unsigned g = (unsigned)((tot + 127) / 128);
+    static const bool exact_sums = [] { const char *e = getenv("CSPQ_LLOYD_EXACT_SUMS"); return !e || atoi(e) != 0; }();
+    const uint8_t *only = nullptr;
+    if (!pf64 && (sub == 8 || sub == 4) && exact_sums) {  // float32 points: the checked parallel sums
+        const unsigned gw = (unsigned)(((int64_t)m * k + 3) / 4);
+        const float *P32 = reinterpret_cast<const float *>(P);
+        uint8_t *redo = L.at<uint8_t>(ws, L.redo);
+        if (sub == 8) sums_exact_kernel<8><<<gw, 128, 0, st>>>(P32, n, m, k, state, b, cnt, start, perm, sums, redo);
+        else sums_exact_kernel<4><<<gw, 128, 0, st>>>(P32, n, m, k, state, b, cnt, start, perm, sums, redo);
+        CSPQ_LAUNCH_CHECK();
+        only = redo;  // the sequential chains below run for the marked clusters only
+    }
     CSPQ_TP_DISPATCH(pf64, P, {
-        if (sub == 8) sums_kernel<8, TP><<<g, 128, 0, st>>>(Pt, n, m, k, sub, state, b, cnt, start, perm, sums);
-        else if (sub == 4) sums_kernel<4, TP><<<g, 128, 0, st>>>(Pt, n, m, k, sub, state, b, cnt, start, perm, sums);
-        else sums_kernel<0, TP><<<g, 128, 0, st>>>(Pt, n, m, k, sub, state, b, cnt, start, perm, sums);
+        if (sub == 8) sums_kernel<8, TP><<<g, 128, 0, st>>>(Pt, n, m, k, sub, state, b, cnt, start, perm, sums, only);
+        else if (sub == 4) sums_kernel<4, TP><<<g, 128, 0, st>>>(Pt, n, m, k, sub, state, b, cnt, start, perm, sums, only);
+        else sums_kernel<0, TP><<<g, 128, 0, st>>>(Pt, n, m, k, sub, state, b, cnt, start, perm, sums, only);
     });
     CSPQ_LAUNCH_CHECK();
     return pairwise_obj(sq, n, b, len, m, state, ws, L, obj, st);

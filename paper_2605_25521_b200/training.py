@@ -79,12 +79,15 @@ def _stack_points(points_list):
     return P, 1
 
 
-def lloyd_iterate_batched(points, init, cfg: TrainConfig, dev=None) -> list[KMeansResult]:
+def lloyd_iterate_batched(points, init, cfg: TrainConfig, dev=None, *,
+                          return_assignments: bool = True) -> list[KMeansResult]:
     """Lloyd from given float64 initial centroids for m subspaces at once.
 
     points: (m, n, sub) array (float32 or float64) or a list of (n, sub);
     init: (m, k, sub) float64.  Each subspace follows training.py:109-159
-    exactly, including its own early stop."""
+    exactly, including its own early stop.  ``return_assignments=False``
+    leaves the final assignments on the device (KMeansResult.assignments is
+    None): callers that only need the codebooks skip an (m, n) int64 copy."""
     N.require_cuda()
     t = torch()
     if isinstance(points, t.Tensor):  # device-resident (m, n, sub) float32/float64
@@ -113,17 +116,18 @@ def lloyd_iterate_batched(points, init, cfg: TrainConfig, dev=None) -> list[KMea
         N.call("cspq_lloyd_train", ptr(Pd), pf64, n, m, sub, k, ptr(Cd), cfg.max_iters, float(cfg.tol),
                ptr(C32), ptr(asg), ptr(objs), ptr(iters), ptr(ws), stream_ptr(dev))
         # assignments leave as one pinned int64 block (widened on the device); results slice it
-        asg64 = t.empty((m, n), dtype=t.int64, pin_memory=True)
-        asg64.copy_(asg.long(), non_blocking=True)
+        if return_assignments:
+            asg64 = t.empty((m, n), dtype=t.int64, pin_memory=True)
+            asg64.copy_(asg.long(), non_blocking=True)
         C32h, objh, ith = (x.cpu().numpy() for x in (C32, objs, iters))
         t.cuda.current_stream(dev).synchronize()
-        asgh = asg64.numpy()
+        asgh = asg64.numpy() if return_assignments else None
     out = []
     for j in range(m):
         it = int(ith[j])
         out.append(KMeansResult(centroids=np.ascontiguousarray(C32h[j]),
                                 objectives=[float(v) for v in objh[j, :it + 1]],
-                                assignments=asgh[j], n_train=n, iterations=it))
+                                assignments=None if asgh is None else asgh[j], n_train=n, iterations=it))
     return out
 
 
@@ -226,7 +230,7 @@ def _sample(points: np.ndarray, cap: int | None, rng: np.random.Generator) -> np
     return points[idx]
 
 
-def _train_many(subspace_points, cfg: TrainConfig, rngs, labels):
+def _train_many(subspace_points, cfg: TrainConfig, rngs, labels, return_assignments: bool = True):
     """Sample, validate, seed and train a list of subspaces together."""
     # every subspace has its own generator, so the draws and gathers run on host threads
     # (numpy releases the GIL in both) with exactly the reference's per-stream draw order
@@ -265,7 +269,7 @@ def _train_many(subspace_points, cfg: TrainConfig, rngs, labels):
     dev = device()
     Pd = to_device(P, dev)
     init = kmeanspp_init_batched(Pd, cfg.k, rngs, dev)
-    return lloyd_iterate_batched(Pd, init, cfg, dev)
+    return lloyd_iterate_batched(Pd, init, cfg, dev, return_assignments=return_assignments)
 
 
 def train_codebook(subvectors: np.ndarray, cfg: TrainConfig, subspace_index: int = 0) -> Codebook:
@@ -291,10 +295,15 @@ def train_codebook_report(subvectors: np.ndarray, cfg: TrainConfig,
 
 
 def train_all_codebooks(dataset, params, cfg: TrainConfig) -> list[Codebook]:
-    return train_all_codebooks_report(dataset, params, cfg)[0]
+    # (the reports' assignments are not returned: they stay on the device)
+    return _train_all(dataset, params, cfg, return_assignments=False)[0]
 
 
 def train_all_codebooks_report(dataset, params, cfg: TrainConfig):
+    return _train_all(dataset, params, cfg, return_assignments=True)
+
+
+def _train_all(dataset, params, cfg: TrainConfig, return_assignments: bool):
     """training.py:203-224: one codebook per subspace from its own sample.
     Accepts a VectorDataset or a raw (n, d) array (the reference's
     ``hasattr(dataset, "data")`` probe mistakes an ndarray's buffer for a
@@ -307,5 +316,5 @@ def train_all_codebooks_report(dataset, params, cfg: TrainConfig):
     # column views: _sample gathers only the sampled rows (the same arrays the reference's
     # per-subspace slice + sample produce, without copying every column block first)
     pts = [data[:, j * sub:(j + 1) * sub] for j in range(params.m)]
-    reports = _train_many(pts, cfg, rngs, range(params.m))
+    reports = _train_many(pts, cfg, rngs, range(params.m), return_assignments)
     return [Codebook.from_rowmajor(j, r.centroids) for j, r in enumerate(reports)], reports
