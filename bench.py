@@ -55,7 +55,7 @@ def parse(argv=None):
     p.add_argument("--mode", default="auto", choices=["auto", "exact", "guarded"])
     p.add_argument("--e2e-rows", type=int, default=0,
                    help="rows per rank through the host API (0 = max(2M, 6 GB of rows), or the whole shard for c5)")
-    p.add_argument("--streams", type=int, default=0, help="host pipeline streams (0 = 3, or 6 for c5)")
+    p.add_argument("--streams", type=int, default=0, help="host pipeline streams (0 = 3, or 2 for c5: 4096-row batches saturate PCIe with two in flight; more only queue -- p50 0.87 ms at 2, 1.81 ms at 6, same vec/s)")
     p.add_argument("--e2e-batch", type=int, default=0,
                    help="host pipeline batch rows (0 = max(131072 rows, 256 MB) capped at a quarter of the sample, "
                         "or 4096 for c5)")
@@ -437,7 +437,7 @@ def e2e_record(cfg, args, X, cs, out, ws, dev, steps, train_fn=None, train_h2d=0
     Xh = P.pinned_empty((ne, cfg.d), np.uint8 if cfg.dtype == "u8" else np.float32)
     Xh[:] = X[:ne].cpu().numpy()
     codes_h = P.pinned_empty((ne, cfg.m), np.uint8)
-    eplan = P.ExecutionPlan(mode=args.mode, batch_rows=batch_rows, streams=args.streams or (6 if cfg.batch else 3))
+    eplan = P.ExecutionPlan(mode=args.mode, batch_rows=batch_rows, streams=args.streams or (2 if cfg.batch else 3))
     nb = (ne + batch_rows - 1) // batch_rows
     bms = np.zeros(nb, np.float64)
     P.encode_dataset_host(Xh, cs, eplan, out=codes_h)  # warm the pipeline
