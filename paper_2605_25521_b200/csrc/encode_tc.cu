@@ -65,7 +65,11 @@ constexpr int kNCls = 9;     // argmin classes = position inside a block of 7 or
 constexpr int kG = 8;        // max tiles per row group (codebook image reuse); the launch picks 1..kG
 constexpr int kGroups = 3;   // epilogue groups: item it belongs to group it % kGroups
 constexpr int kNA = kGroups; // A-operand stages (a group writes item it + kGroups into item it's stage)
-constexpr int kThreads = 64 + 128 * kGroups;  // MMA warp, loader warp, kGroups x 4 epilogue warps
+constexpr int kThreads = 128 + 128 * kGroups;  // warpgroup 0 = MMA warp, loader warp, two idle warps; then
+                                               // kGroups epilogue warpgroups.  Warpgroup 0 hands its
+                                               // registers to the epilogue (setmaxnreg kRegsLight / kRegsEpi)
+constexpr int kRegsLight = 40, kRegsEpi = 152;  // 128 x 40 + 384 x 152 = 63,488 <= 65,536
+static_assert(128 * kRegsLight + 128 * kGroups * kRegsEpi <= 65536, "register pool");
 constexpr int kNC = 1;        // accumulator chunks per item (N = 256 / kNC per MMA, own commit + barriers):
                               // MMA and scan overlap chunk by chunk; measured on c3: 1 = 2.16e8 vec/s,
                               // 2 = 2.04e8, 4 = 1.44e8 (an N=64 MMA costs almost what an N=256 one does);
@@ -73,8 +77,6 @@ constexpr int kNC = 1;        // accumulator chunks per item (N = 256 / kNC per 
 constexpr int kCW = 256 / kNC;  // chunk width in TMEM columns (a multiple of 64: one tcgen05.ld x64)
 constexpr int kPD = 2;        // cp.async prefetch distance, in the group's own items
 constexpr int kRing = 3;      // x slots per group (> kPD: an item's slot outlives its fix-up)
-constexpr int kScrW = 36;     // floats per row of the block-minima scratch: 32 + 4 pad, so the 16-B
-                              // stores / loads of 8 consecutive rows hit 8 distinct bank quads
 
 // error constant E of the tensor scores: |S - s_oracle| <= E W, W = max|b| + ||x|| max||c||
 // (tf32 split, 2 roundings per K = 8 step, the oracle's own chain; 1 % slack).  Lloyd's final
@@ -108,17 +110,28 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 }
 // bounded wait: a lost arrival traps (error) instead of hanging the device
 constexpr uint32_t kSuspendNs = 1000000;
+__device__ __noinline__ long long mbar_wait_check(long long t0) {
+    // every 256th unsuccessful try: ~10 s of clock without the phase flip is a lost arrival (not a
+    // time slice)
+    const long long t = clock64();
+    if (t0 == 0) return t;
+    if (t - t0 > 20000000000ll) __trap();
+    return t0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t done = 0;
+    // suspend (woken by the phase flip) instead of busy polling: spinning warps steal issue slots
+    // from the epilogue warps that share their SM sub-partition.  A suspended try_wait also
+    // returns on other barrier traffic of the CTA (~5 times per wait, ncu source counters), so the
+    // retry path is kept to the try itself plus a counter: the clock is read every 256th retry
+    const uint32_t addr = smem_u32(bar);
+    uint32_t spins = 0;
     long long t0 = 0;
-    for (bool first = true;; first = false) {
-        // suspend (woken by the phase flip) instead of busy polling: spinning warps steal
-        // issue slots from the epilogue warps that share their SM sub-partition
+    for (;;) {
+        uint32_t done;
         asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity), "r"(kSuspendNs) : "memory");
+                     : "=r"(done) : "r"(addr), "r"(parity), "r"(kSuspendNs) : "memory");
         if (done) return;
-        if (first) t0 = clock64();  // (the clock is read only once a wait actually waits)
-        else if (clock64() - t0 > 20000000000ll) __trap();  // ~10 s: a lost arrival (not a time slice)
+        if ((++spins & 255u) == 0) t0 = mbar_wait_check(t0);
     }
 }
 __device__ __forceinline__ bool elect_one() {
@@ -233,8 +246,7 @@ struct TcSmem {
     static constexpr size_t oA = oB + 2 * (size_t)S::kBBytes;
     static constexpr size_t oC = oA + kNA * (size_t)S::kABytes;
     static constexpr size_t oX = oC + 2 * (size_t)kCFloats * 4;
-    static constexpr size_t oS = oX + kGroups * kRing * (size_t)kXBytes;  // block-minima scratch [kGroups][kTM][kScrW]
-    static constexpr size_t oG = oS + (size_t)kGroups * kTM * kScrW * 4;     // guard constants (2 m floats)
+    static constexpr size_t oG = oX + kGroups * kRing * (size_t)kXBytes;  // guard constants (2 m floats)
     static size_t total(int m) { return oG + ((size_t)2 * m * 4 + 15) / 16 * 16 + sizeof(TcSmemHdr) + 16; }
 };
 
@@ -275,16 +287,22 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
     float *sC = reinterpret_cast<float *>(smem_raw + L::oC);
     unsigned char *sX = smem_raw + L::oX;
     float *sGuard = reinterpret_cast<float *>(smem_raw + L::oG);
-    float *sScr = reinterpret_cast<float *>(smem_raw + L::oS);
     TcSmemHdr *H = reinterpret_cast<TcSmemHdr *>(smem_raw + L::oG + ((size_t)2 * m * 4 + 15) / 16 * 16);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t ntiles = (n + kTM - 1) / kTM;
+    const int ntiles = (int)((n + kTM - 1) / kTM);  // (< 2^31: checked by the launch)
     const int64_t ngroups = (ntiles + gs - 1) / gs;
     // contiguous pair ranges balance the SMs at pair granularity (a whole row group per CTA
     // left up to a row group's worth of items of imbalance: c1's 782 tiles)
     const int64_t npairs = ngroups * m;
-    const int p_begin = (int)(npairs * blockIdx.x / gridDim.x), p_end = (int)(npairs * (blockIdx.x + 1) / gridDim.x);
+    // (computed inside each role's region, from an opaque zero: a value born before setmaxnreg and
+    // live across it is given a stack slot by ptxas, and the pair counters would live there)
+    auto pair_range = [&](int &p_begin, int &p_end) {
+        unsigned z;
+        asm volatile("mov.u32 %0, 0;" : "=r"(z));
+        p_begin = (int)(npairs * (blockIdx.x + z) / gridDim.x);
+        p_end = (int)(npairs * (blockIdx.x + z + 1) / gridDim.x);
+    };
 
     for (int i = threadIdx.x; i < 2 * m; i += kThreads) sGuard[i] = guard[i];
     if (threadIdx.x == 0) {
@@ -309,16 +327,22 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = H->tmem_base;
-
+    // the MMA / loader warpgroup keeps kRegsLight registers per thread; the epilogue warpgroups take
+    // what it frees (the block minima of a whole item then stay in registers: no shared-memory scratch)
+    // (each role's code is dominated by its own setmaxnreg: ptxas budgets registers per region)
+    if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsLight));
     if (warp == 0) {
         // ---------------- MMA issuer ----------------
         // The whole warp walks the items (warp-uniform descriptors live in uniform registers) and
         // one elected lane issues: no per-thread -> uniform register waterfall around each MMA
         // (scripts/micro/umma_rate.cu: 676 vs 756 cycles from issue to completion of an item).
         uint32_t it = 0, jt = 0;
+        int p_begin, p_end;
+        pair_range(p_begin, p_end);
         for (int p = p_begin; p < p_end; ++p, ++jt) {
             const int g = p / m;
-            const int64_t t0 = (int64_t)g * gs, tn = (ntiles - t0 < gs) ? (ntiles - t0) : gs;
+            const int tn = min(ntiles - g * gs, gs);
             {
                 const int jb = jt & 1;
                 mbar_wait(&H->b_full[jb], (jt >> 1) & 1);
@@ -352,8 +376,23 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         }
     } else if (warp == 1) {
         // ---------------- codebook loader: tf32 image (MMA) + fp32 codebook (fix-up) ----------------
+#ifdef CSPQ_TC_STAMPS
+        if (lane == 1 && stamp) {
+            for (uint32_t it = 0; it < kStampItems; ++it) {
+                uint32_t done = 0;
+                long long t0 = clock64();
+                while (!done && clock64() - t0 < 4000000) {
+                    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                                 : "=r"(done) : "r"(smem_u32(&H->t_full[it & 3][0])), "r"((it >> 2) & 1) : "memory");
+                }
+                stamp[it * 8 + 3] = clock64();
+            }
+        }
+#endif
         if (lane == 0) {
             uint32_t jt = 0;
+            int p_begin, p_end;
+            pair_range(p_begin, p_end);
             for (int p = p_begin; p < p_end; ++p) {
                 {
                     const int j = p % m;
@@ -368,16 +407,17 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 }
             }
         }
+    }
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
         // ---------------- epilogue + A producer: kGroups groups of 4 warps ----------------
         // Group e owns the items with item % kGroups == e (TMEM buffer item & 1).  Thread (q, lane)
         // owns tile row r = 32 q + lane: it reads that TMEM lane, and it also writes that
         // row of the A operand of the group's next item (item + kGroups) and prefetches the
         // row's x kPD owned items ahead into the group's x ring.
-        const int e = (warp - 2) >> 2;  // group: items it with it % kGroups == e
+        const int e = (warp - 4) >> 2;  // group: items it with it % kGroups == e
         const int q = warp & 3;
         const int r = 32 * q + lane;
-        float *scratch = sScr + ((size_t)e * kTM + r) * kScrW;  // this thread's 32 block minima
         constexpr float kE = tc_error_constant(SUB);
         static_assert(S::kSteps == (SUB == 8 ? 4 : 2), "tc_error_constant counts K = 8 MMA steps");
         // the group's x ring: owned item k (item e + kGroups k) lives in slot k % kRing
@@ -464,7 +504,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 
         // The group walks its own items only (item e, e + kGroups, ...); ic / ip run kGroups
         // and kGroups kPD items ahead for the A conversion and the x prefetch.
-        ItemIter ii(p_begin, p_end, m, gs, (int)ntiles);
+        int p_begin, p_end;
+        pair_range(p_begin, p_end);
+        ItemIter ii(p_begin, p_end, m, gs, ntiles);
         ii.advance(e);
         ItemIter ip = ii;
         for (int d = 0; d < kPD; ++d, ip.advance(kGroups)) prefetch(ip, d);
@@ -488,7 +530,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
             const int j = ii.j;
-            float cls[kNCls];
+            float cls[kNCls], bm[32];
 #pragma unroll
             for (int c = 0; c < kNCls; ++c) cls[c] = pos_inf_f();
 #pragma unroll
@@ -505,6 +547,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 if (ch % kLdPerChunk == kLdPerChunk - 1) {  // chunk c is in registers: hand it back
                     tc_fence_before();
                     mbar_arrive(&H->t_empty[it & 3][c]);
+                    if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 4] = clock64();
                 }
 #define SV(i) __uint_as_float(v[(i)])
                 if (probe & 8) {
@@ -514,7 +557,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 // each 16 columns = a block of 7 then a block of 9 (3 + 4 three-input minima, no
                 // idle operand slot); the class is the position inside the block, so classes 0-6
                 // take two columns per 16 and classes 7-8 one (paired across 16-column groups)
-                float bmc[8];
+                float *bmc = bm + 8 * ch;
 #pragma unroll
                 for (int bp = 0; bp < 4; ++bp) {
                     const int o = 16 * bp;
@@ -528,8 +571,6 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                     bmc[2 * bp + 1] = fmin3(fmin3(SV(o + 7), SV(o + 8), SV(o + 9)), fmin3(SV(o + 10), SV(o + 11), SV(o + 12)),
                                             fmin3(SV(o + 13), SV(o + 14), SV(o + 15)));
                 }
-                reinterpret_cast<float4 *>(scratch + 8 * ch)[0] = make_float4(bmc[0], bmc[1], bmc[2], bmc[3]);
-                reinterpret_cast<float4 *>(scratch + 8 * ch)[1] = make_float4(bmc[4], bmc[5], bmc[6], bmc[7]);
 #undef SV
             }
             if (probe & 1) {  // (timing probe: no TMEM reads; still walk the barriers)
@@ -554,12 +595,6 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 if (row < n && !(probe & 64)) codes[row * cs + j * cjs] = (uint8_t)(__float_as_uint(cls[0] + xnorm) & 255);
                 continue;
             }
-            float bm[32];
-#pragma unroll
-            for (int b4 = 0; b4 < 8; ++b4) {
-                const float4 t4 = reinterpret_cast<const float4 *>(scratch)[b4];
-                bm[4 * b4] = t4.x; bm[4 * b4 + 1] = t4.y; bm[4 * b4 + 2] = t4.z; bm[4 * b4 + 3] = t4.w;
-            }
             // Final selection on the FMA pipe.  m1 = the minimum (of the class minima); the band
             // indicator ind(v) = sat(1 - (v - m1) / (4 E W)) is exactly 1 for v == m1, exactly 0
             // beyond the guard band and in between inside it (0 for NaN).  A (row, subspace) is
@@ -572,26 +607,45 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             // the 2 E W that exactness needs.)
             const float m1 = fmin3(fmin3(cls[0], cls[1], cls[2]), fmin3(cls[3], cls[4], cls[5]), fmin3(cls[6], cls[7], cls[8]));
             const float W = sGuard[2 * j] + xnorm * sGuard[2 * j + 1];
-            float kinv;
-            asm("rcp.approx.f32 %0, %1;" : "=f"(kinv) : "f"(4.0f * kE * W));  // inf for W = 0: every ind = 0 (flag)
-            float qcf = 0.f, ncf = 0.f, wbf = 0.f, nbf = 0.f;
+            // second level over the 32 block minima: slot b = 8 u + s; 4 "super-block" minima (u)
+            // and 8 "super-class" minima (s) -- two blocks differ in u or in s, so a second block
+            // inside the band shows up in another super-block or super-class minimum
+            float sbm[4], scm[8];
 #pragma unroll
-            for (int c = 0; c < kNCls; ++c) {
-                const float ind = __saturatef(__fmaf_rn(__fsub_rn(cls[c], m1), -kinv, 1.0f));
-                qcf = __fmaf_rn(ind, (float)(c + 8), qcf);
-                ncf = __fadd_rn(ncf, ind);
-            }
+            for (int u = 0; u < 4; ++u)
+                sbm[u] = fmin3(fmin3(bm[8 * u], bm[8 * u + 1], bm[8 * u + 2]), fmin3(bm[8 * u + 3], bm[8 * u + 4], bm[8 * u + 5]),
+                               fminf(bm[8 * u + 6], bm[8 * u + 7]));
 #pragma unroll
-            for (int b = 0; b < 32; ++b) {
-                const float ind = __saturatef(__fmaf_rn(__fsub_rn(bm[b], m1), -kinv, 1.0f));
-                wbf = __fmaf_rn(ind, (float)(b + 32), wbf);
-                nbf = __fadd_rn(nbf, ind);
-            }
+            for (int c = 0; c < 8; ++c) scm[c] = fmin3(fmin3(bm[c], bm[8 + c], bm[16 + c]), bm[24 + c], bm[24 + c]);
+            // binary band indicator on the FMA pipe: ind(v) = sat((thr - v) 2^126), thr = m1 + 4 E W;
+            // the difference is flushed to zero below 2^-126, so ind is exactly 1 (v < thr) or 0
+            // (v >= thr, NaN, or W = 0 / non-finite).  One exact integer accumulator counts and
+            // names the candidates inside the band: class c adds 2^9 + c, super-class s adds
+            // 2^13 + 16 s, super-block u adds 2^17 + 128 u.  The minimum itself is always inside, so
+            // every count is >= 1 and carries only ever raise a count: the sum lies in
+            // [kSelBase, kSelBase + 512) iff exactly one candidate of each kind is inside the band,
+            // and its low 9 bits then hold (u, s, c).
+            const float thr = __fadd_rn(m1, 4.0f * kE * W);
+            auto ind = [&](float v) {
+                float d, o;
+                asm("sub.ftz.f32 %0, %1, %2;" : "=f"(d) : "f"(thr), "f"(v));
+                asm("mul.sat.f32 %0, %1, 0f7E800000;" : "=f"(o) : "f"(d));  // x 2^126
+                return o;
+            };
+            constexpr int kSelBase = (1 << 9) + (1 << 13) + (1 << 17);
+            float tc = 0.f, ts = 0.f, tu = 0.f;
+#pragma unroll
+            for (int c = 0; c < kNCls; ++c) tc = __fmaf_rn(ind(cls[c]), (float)((1 << 9) + c), tc);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) ts = __fmaf_rn(ind(scm[c]), (float)((1 << 13) + 16 * c), ts);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) tu = __fmaf_rn(ind(sbm[u]), (float)((1 << 17) + 128 * u), tu);
+            const uint32_t sel = (uint32_t)(__float2int_rz(__fadd_rn(__fadd_rn(tc, ts), tu)) - kSelBase);
             const int64_t row = ii.tile() * kTM + r;
             // block slot sb starts at column 8 sb - (sb & 1) (7-blocks at even slots, 9-blocks at odd)
-            const int sb = __float2int_rz(wbf) - 32;
-            int code = 8 * sb - (sb & 1) + (__float2int_rz(qcf) - 8);
-            const bool flag = (row < n) && !(ncf == 1.0f && nbf == 1.0f);
+            const int sb = (int)(sel >> 4) & 31;
+            int code = 8 * sb - (sb & 1) + (int)(sel & 15);
+            const bool flag = (row < n) && !(sel < 512u);
             // exact warp-cooperative re-encode of flagged rows (x and the fp32 codebook from
             // shared memory: the item's x slot stays valid until kPD more owned items)
             if constexpr (kMark) {  // mark mode (Lloyd screening): flagged rows are settled by the caller

@@ -19,7 +19,7 @@ for _ in range(2):
     P.encode_dataset_device(X, cs, P.ExecutionPlan(mode="tensor"), best=best)
 torch.cuda.synchronize()
 st = best.view(torch.int64).flatten()[:2048 * 8].cpu().numpy().reshape(2048, 8).astype(np.float64)
-names = ["mma_afull", "mma_tempty", "mma_commit", "unused3", "unused4", "epi_tfull", "epi_release", "epi_done"]
+names = ["mma_afull", "mma_tempty", "mma_commit", "obs_tfull", "epi_arrive", "epi_tfull", "epi_release", "epi_done"]
 base = st[0, 0]
 st = st - base
 for i in list(range(0, 12)) + list(range(1000, 1012)):
@@ -27,4 +27,5 @@ for i in list(range(0, 12)) + list(range(1000, 1012)):
 d = np.diff(st[200:1800], axis=0)
 print("median per-item deltas:", {names[k]: float(np.median(d[:, k])) for k in range(8)})
 print("median epi tfull->release", float(np.median((st[200:1800, 6] - st[200:1800, 5]))), "release->done", float(np.median(st[200:1800, 7] - st[200:1800, 6])))
+print("median first-issue(tempty)->obs_tfull", float(np.median(st[200:1800, 3] - st[200:1800, 1])), "obs_tfull->epi_tfull", float(np.median(st[200:1800, 5] - st[200:1800, 3])), "epi_tfull->arrive", float(np.median(st[200:1800, 4] - st[200:1800, 5])), "arrive(it)->mma_tempty(it+2)", float(np.median(st[202:1800, 1] - st[200:1798, 4])))
 print("median mma tempty wait (tempty - afull)", float(np.median(st[200:1800, 1] - st[200:1800, 0])), "commit->epi tfull", float(np.median(st[200:1800, 5] - st[200:1800, 2])))
