@@ -64,7 +64,10 @@ constexpr int kN = 256;      // centroids (MMA N)
 constexpr int kNCls = 9;     // argmin classes = position inside a block of 7 or 9 centroids
 constexpr int kG = 8;        // max tiles per row group (codebook image reuse); the launch picks 1..kG
 constexpr int kGroups = 3;   // epilogue groups: item it belongs to group it % kGroups
-constexpr int kNA = kGroups; // A-operand stages (a group writes item it + kGroups into item it's stage)
+constexpr int kNA = 2 * kGroups;  // A-operand stages: a group alternates between two, so it writes the A rows of
+                                  // its next item (it + kGroups) before it waits for item it's accumulator --
+                                  // with one stage per group the next item's MMA could only start after the
+                                  // current item's scan (the chain scan -> A rows -> MMA -> scan bounded a group)
 constexpr int kThreads = 128 + 128 * kGroups;  // warpgroup 0 = MMA warp, loader warp, two idle warps; then
                                                // kGroups epilogue warpgroups.  Warpgroup 0 hands its
                                                // registers to the epilogue (setmaxnreg kRegsLight / kRegsEpi)
@@ -290,16 +293,15 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
     TcSmemHdr *H = reinterpret_cast<TcSmemHdr *>(smem_raw + L::oG + ((size_t)2 * m * 4 + 15) / 16 * 16);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntiles = (int)((n + kTM - 1) / kTM);  // (< 2^31: checked by the launch)
-    const int64_t ngroups = (ntiles + gs - 1) / gs;
-    // contiguous pair ranges balance the SMs at pair granularity (a whole row group per CTA
-    // left up to a row group's worth of items of imbalance: c1's 782 tiles)
-    const int64_t npairs = ngroups * m;
-    // (computed inside each role's region, from an opaque zero: a value born before setmaxnreg and
-    // live across it is given a stack slot by ptxas, and the pair counters would live there)
-    auto pair_range = [&](int &p_begin, int &p_end) {
+    // The walk's constants are computed inside each role's region, from an opaque zero: a value
+    // born before setmaxnreg and live across it is given a stack slot by ptxas, and the tile / pair
+    // counters would live there.  Contiguous pair ranges balance the SMs at pair granularity (a
+    // whole row group per CTA left up to a row group's worth of items of imbalance: c1's 782 tiles)
+    auto pair_range = [&](int &p_begin, int &p_end, int &ntiles) {
         unsigned z;
         asm volatile("mov.u32 %0, 0;" : "=r"(z));
+        ntiles = (int)((n + z + kTM - 1) / kTM);  // (< 2^31: checked by the launch)
+        const int64_t npairs = (int64_t)((ntiles + gs - 1) / gs) * m;
         p_begin = (int)(npairs * (blockIdx.x + z) / gridDim.x);
         p_end = (int)(npairs * (blockIdx.x + z + 1) / gridDim.x);
     };
@@ -338,8 +340,8 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         // one elected lane issues: no per-thread -> uniform register waterfall around each MMA
         // (scripts/micro/umma_rate.cu: 676 vs 756 cycles from issue to completion of an item).
         uint32_t it = 0, jt = 0;
-        int p_begin, p_end;
-        pair_range(p_begin, p_end);
+        int p_begin, p_end, ntiles;
+        pair_range(p_begin, p_end, ntiles);
         for (int p = p_begin; p < p_end; ++p, ++jt) {
             const int g = p / m;
             const int tn = min(ntiles - g * gs, gs);
@@ -348,23 +350,37 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 mbar_wait(&H->b_full[jb], (jt >> 1) & 1);
                 for (int t = 0; t < tn; ++t, ++it) {
                     const int as = it % kNA, tb = it & 1;
+                    // everything the issue needs is computed before the waits: after the accumulator
+                    // is handed back only the fence, the MMAs and the commit remain
+                    const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
+                    uint64_t da[S::kSteps], db[kNC][S::kSteps];
+#pragma unroll
+                    for (int s = 0; s < S::kSteps; ++s) {
+                        da[s] = make_desc(a0 + 2 * s * 128, 128, S::kRowGroupBytes);
+#pragma unroll
+                        for (int c = 0; c < kNC; ++c)  // centroids c kCW ..
+                            db[c][s] = make_desc(b0 + (uint32_t)(c * (kCW / 8) * S::kRowGroupBytes) + 2 * s * 128, 128, S::kRowGroupBytes);
+                    }
+                    const uint32_t tacc = tmem + tb * kN;
+                    uint64_t *const tfull = &H->t_full[it & 3][0], *const tempty = &H->t_empty[(it - 2) & 3][0];
+                    const uint32_t tepar = ((it - 2) >> 2) & 1;
                     mbar_wait(&H->a_full[as], (it / kNA) & 1);
                     if (stamp && lane == 0 && it < kStampItems) stamp[it * 8 + 0] = clock64();
-                    const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
+#pragma unroll
                     for (int c = 0; c < kNC; ++c) {
                         // chunk c of buffer tb drained by the scan of item it - 2
-                        if (it >= 2) mbar_wait(&H->t_empty[(it - 2) & 3][c], ((it - 2) >> 2) & 1);
+                        if (it >= 2) mbar_wait(tempty + c, tepar);
                         if (stamp && lane == 0 && c == 0 && it < kStampItems) stamp[it * 8 + 1] = clock64();
                         tc_fence_after();
-                        const uint32_t bc = b0 + (uint32_t)(c * (kCW / 8) * S::kRowGroupBytes);  // centroids c kCW ..
                         if (elect_one()) {
 #pragma unroll
                             for (int s = 0; s < S::kSteps; ++s) {
-                                const uint64_t da = make_desc(a0 + 2 * s * 128, 128, S::kRowGroupBytes);
-                                const uint64_t db = make_desc(bc + 2 * s * 128, 128, S::kRowGroupBytes);
-                                if (!(probe & 2)) mma_tf32(tmem + tb * kN + c * kCW, da, db, s > 0);
+#ifdef CSPQ_TC_PROBES
+                                if ((probe & 256) && s >= S::kSteps / 2) break;  // (timing probe: half the MMAs)
+#endif
+                                if (!(probe & 2)) mma_tf32(tacc + c * kCW, da[s], db[c][s], s > 0);
                             }
-                            mma_commit(&H->t_full[it & 3][c]);  // the last one also frees A stage `as`
+                            mma_commit(tfull + c);  // the last one also frees A stage `as`
                         }
                         __syncwarp();
                     }
@@ -391,8 +407,8 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 #endif
         if (lane == 0) {
             uint32_t jt = 0;
-            int p_begin, p_end;
-            pair_range(p_begin, p_end);
+            int p_begin, p_end, ntiles;
+            pair_range(p_begin, p_end, ntiles);
             for (int p = p_begin; p < p_end; ++p) {
                 {
                     const int j = p % m;
@@ -443,10 +459,10 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             }
             cp_async_commit();
         };
-        // A row of the group's next item (A stage e: the group's items are all == e mod kNA) from
+        // A row of one of the group's items (A stage = item % kNA: e or e + kGroups) from
         // the staged x of ring slot `slot`; returns ||x|| rounded up
-        static_assert(kNA == kGroups, "A stage = item % kNA = the group index");
-        auto convert = [&](int slot) -> float {
+        static_assert(kNA == 2 * kGroups, "A stage = item % kNA: the group's items alternate between e and e + kGroups");
+        auto convert = [&](int slot, int stage) -> float {
             const TIn *xr = reinterpret_cast<const TIn *>(ring(slot));
             float x[SUB];
             if constexpr (sizeof(TIn) == 4) {
@@ -476,7 +492,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 ss = __fmaf_rn(x[tt], x[tt], ss);
             }
             if (!(probe & 4)) {
-                unsigned char *rowp = sA + e * S::kABytes + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16;
+                unsigned char *rowp = sA + stage * S::kABytes + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16;
                 auto st = [&](int c, float a0, float a1, float a2, float a3) {
                     *reinterpret_cast<float4 *>(rowp + c * 128) = make_float4(a0, a1, a2, a3);
                 };
@@ -491,7 +507,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 }
             }
             fence_proxy_async();
-            mbar_arrive(&H->a_full[e]);
+            mbar_arrive(&H->a_full[stage]);
             return __fsqrt_ru(ss) * 1.000001f;
         };
         // b_empty[p & 1] phase p >> 1 belongs to pair p.  A group that owns no item of
@@ -504,14 +520,14 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 
         // The group walks its own items only (item e, e + kGroups, ...); ic / ip run kGroups
         // and kGroups kPD items ahead for the A conversion and the x prefetch.
-        int p_begin, p_end;
-        pair_range(p_begin, p_end);
+        int p_begin, p_end, ntiles;
+        pair_range(p_begin, p_end, ntiles);
         ItemIter ii(p_begin, p_end, m, gs, ntiles);
         ii.advance(e);
         ItemIter ip = ii;
         for (int d = 0; d < kPD; ++d, ip.advance(kGroups)) prefetch(ip, d);
         float norm_cur = 0.f;
-        if (ii.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(0); }
+        if (ii.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(0, e); }
         ItemIter ic = ii;
         ic.advance(kGroups);
         uint32_t rel = 0;  // pairs below rel are released by this thread
@@ -527,12 +543,27 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         for (uint32_t it = e; ii.valid(); it += kGroups, ii.advance(kGroups), ic.advance(kGroups), ip.advance(kGroups),
                                           rotate()) {
             for (; rel < ii.jt; ++rel) release_pair(rel);  // done with those pairs' sC
+            // the group's next item first: stage the x prefetch of the one after it and write its A
+            // rows into the group's other A stage (free since item it - kGroups was scanned), so
+            // its MMA can start as soon as a TMEM buffer is handed back
+            if (!(probe & 32)) prefetch(ip, s_pf);  // (an empty group keeps the wait count uniform)
+            float norm_next = 0.f;
+            if (ic.valid()) {
+                if (!(probe & 32)) cp_async_wait<kPD - 1>();
+                norm_next = convert(s_next, (int)((it + kGroups) % kNA));
+            }
             const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
             const int j = ii.j;
-            float cls[kNCls], bm[32];
+            // second level over the 32 block minima (slot b = 4 u + s), folded chunk by chunk: 8
+            // "super-block" minima (u = b >> 2) and 4 "super-class" minima (s = b & 3) -- two blocks
+            // differ in u or in s, so a second block inside the band shows up in another super-block
+            // or super-class minimum
+            float cls[kNCls], sbm[8], scm[4];
 #pragma unroll
             for (int c = 0; c < kNCls; ++c) cls[c] = pos_inf_f();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) scm[c] = pos_inf_f();
 #pragma unroll
             for (int ch = 0; ch < 4 && !(probe & 1); ++ch) {
                 constexpr int kLdPerChunk = kCW / 64;
@@ -557,7 +588,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 // each 16 columns = a block of 7 then a block of 9 (3 + 4 three-input minima, no
                 // idle operand slot); the class is the position inside the block, so classes 0-6
                 // take two columns per 16 and classes 7-8 one (paired across 16-column groups)
-                float *bmc = bm + 8 * ch;
+                float bmc[8];
 #pragma unroll
                 for (int bp = 0; bp < 4; ++bp) {
                     const int o = 16 * bp;
@@ -571,6 +602,11 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                     bmc[2 * bp + 1] = fmin3(fmin3(SV(o + 7), SV(o + 8), SV(o + 9)), fmin3(SV(o + 10), SV(o + 11), SV(o + 12)),
                                             fmin3(SV(o + 13), SV(o + 14), SV(o + 15)));
                 }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    sbm[2 * ch + h] = fmin3(fmin3(bmc[4 * h], bmc[4 * h + 1], bmc[4 * h + 2]), bmc[4 * h + 3], bmc[4 * h + 3]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) scm[c] = fmin3(scm[c], bmc[c], bmc[4 + c]);
 #undef SV
             }
             if (probe & 1) {  // (timing probe: no TMEM reads; still walk the barriers)
@@ -580,14 +616,6 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 }
             }
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 6] = clock64();
-            // the group's next item: stage its x prefetch and write its A operand now, so
-            // its MMA can start as soon as the other group's item is done
-            if (!(probe & 32)) prefetch(ip, s_pf);  // (an empty group keeps the wait count uniform)
-            float norm_next = 0.f;
-            if (ic.valid()) {
-                if (!(probe & 32)) cp_async_wait<kPD - 1>();
-                norm_next = convert(s_next);
-            }
             const float xnorm = norm_cur;
             norm_cur = norm_next;
             if (probe & 128) {  // (timing probe: no selection / fix-up; garbage codes)
@@ -607,21 +635,11 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             // the 2 E W that exactness needs.)
             const float m1 = fmin3(fmin3(cls[0], cls[1], cls[2]), fmin3(cls[3], cls[4], cls[5]), fmin3(cls[6], cls[7], cls[8]));
             const float W = sGuard[2 * j] + xnorm * sGuard[2 * j + 1];
-            // second level over the 32 block minima: slot b = 8 u + s; 4 "super-block" minima (u)
-            // and 8 "super-class" minima (s) -- two blocks differ in u or in s, so a second block
-            // inside the band shows up in another super-block or super-class minimum
-            float sbm[4], scm[8];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                sbm[u] = fmin3(fmin3(bm[8 * u], bm[8 * u + 1], bm[8 * u + 2]), fmin3(bm[8 * u + 3], bm[8 * u + 4], bm[8 * u + 5]),
-                               fminf(bm[8 * u + 6], bm[8 * u + 7]));
-#pragma unroll
-            for (int c = 0; c < 8; ++c) scm[c] = fmin3(fmin3(bm[c], bm[8 + c], bm[16 + c]), bm[24 + c], bm[24 + c]);
             // binary band indicator on the FMA pipe: ind(v) = sat((thr - v) 2^126), thr = m1 + 4 E W;
             // the difference is flushed to zero below 2^-126, so ind is exactly 1 (v < thr) or 0
             // (v >= thr, NaN, or W = 0 / non-finite).  One exact integer accumulator counts and
             // names the candidates inside the band: class c adds 2^9 + c, super-class s adds
-            // 2^13 + 16 s, super-block u adds 2^17 + 128 u.  The minimum itself is always inside, so
+            // 2^13 + 16 s, super-block u adds 2^17 + 64 u.  The minimum itself is always inside, so
             // every count is >= 1 and carries only ever raise a count: the sum lies in
             // [kSelBase, kSelBase + 512) iff exactly one candidate of each kind is inside the band,
             // and its low 9 bits then hold (u, s, c).
@@ -637,9 +655,9 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 #pragma unroll
             for (int c = 0; c < kNCls; ++c) tc = __fmaf_rn(ind(cls[c]), (float)((1 << 9) + c), tc);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) ts = __fmaf_rn(ind(scm[c]), (float)((1 << 13) + 16 * c), ts);
+            for (int c = 0; c < 4; ++c) ts = __fmaf_rn(ind(scm[c]), (float)((1 << 13) + 16 * c), ts);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) tu = __fmaf_rn(ind(sbm[u]), (float)((1 << 17) + 128 * u), tu);
+            for (int u = 0; u < 8; ++u) tu = __fmaf_rn(ind(sbm[u]), (float)((1 << 17) + 64 * u), tu);
             const uint32_t sel = (uint32_t)(__float2int_rz(__fadd_rn(__fadd_rn(tc, ts), tu)) - kSelBase);
             const int64_t row = ii.tile() * kTM + r;
             // block slot sb starts at column 8 sb - (sb & 1) (7-blocks at even slots, 9-blocks at odd)
