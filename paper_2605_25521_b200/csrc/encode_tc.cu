@@ -90,12 +90,12 @@ __host__ __device__ constexpr float tc_error_constant(int sub) {
 
 template <int SUB>
 struct TcShape {
-    static constexpr int K = SUB == 8 ? 32 : 16;    // tf32 elements per operand row
-    static constexpr int kChunks = K / 4;           // 16-byte chunks per row
-    static constexpr int kSteps = K / 8;            // MMAs (K = 8 each)
+    static constexpr int K = SUB == 8 ? 32 : 16;    // fp16 elements per operand row
+    static constexpr int kChunks = K / 8;           // 16-byte chunks (8 fp16) per row
+    static constexpr int kSteps = K / 16;           // MMAs (kind::f16, K = 16 each)
     static constexpr int kRowGroupBytes = kChunks * 128;  // 8 rows x all chunks
-    static constexpr int kABytes = kTM * K * 4;
-    static constexpr int kBBytes = kN * K * 4;
+    static constexpr int kABytes = kTM * K * 2;
+    static constexpr int kBBytes = kN * K * 2;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -164,14 +164,14 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 __host__ __device__ constexpr uint32_t make_idesc(int n = kN) {
-    // kind::tf32: D f32 (bit 4), A tf32 (2 << 7), B tf32 (2 << 10), K-major A/B,
+    // kind::f16: D f32 (bit 4), A f16 (0 << 7), B f16 (0 << 10), K-major A/B,
     // N >> 3 at [17, 23), M >> 4 at [24, 29)
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+    return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
                  "l"(da), "l"(db), "r"(make_idesc(kCW)), "r"(accumulate) : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
@@ -191,10 +191,22 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
 }
 #undef CSPQ_LD8
 
-__device__ __forceinline__ float tf32_rna(float x) {
+// two floats -> packed fp16 (round to nearest even; beyond the fp16 range -> inf, which makes the
+// scores NaN and the row flagged); lo is the element at the lower address
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
     uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ float f16_lo(uint32_t v) {
+    float f;
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tcvt.f32.f16 %0, l;\n\t}" : "=f"(f) : "r"(v));
+    return f;
+}
+__device__ __forceinline__ float f16_hi(uint32_t v) {
+    float f;
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tcvt.f32.f16 %0, h;\n\t}" : "=f"(f) : "r"(v));
+    return f;
 }
 
 template <int SUB>
@@ -249,8 +261,8 @@ struct TcSmem {
     static constexpr size_t oA = oB + 2 * (size_t)S::kBBytes;
     static constexpr size_t oC = oA + kNA * (size_t)S::kABytes;
     static constexpr size_t oX = oC + 2 * (size_t)kCFloats * 4;
-    static constexpr size_t oG = oX + kGroups * kRing * (size_t)kXBytes;  // guard constants (2 m floats)
-    static size_t total(int m) { return oG + ((size_t)2 * m * 4 + 15) / 16 * 16 + sizeof(TcSmemHdr) + 16; }
+    static constexpr size_t oG = oX + kGroups * kRing * (size_t)kXBytes;  // per subspace: band constants, scale (float4)
+    static size_t total(int m) { return oG + (size_t)m * 16 + sizeof(TcSmemHdr) + 16; }
 };
 
 // ------------------------------------------------------------------ the kernel
@@ -289,8 +301,8 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
     unsigned char *sA = smem_raw + L::oA;
     float *sC = reinterpret_cast<float *>(smem_raw + L::oC);
     unsigned char *sX = smem_raw + L::oX;
-    float *sGuard = reinterpret_cast<float *>(smem_raw + L::oG);
-    TcSmemHdr *H = reinterpret_cast<TcSmemHdr *>(smem_raw + L::oG + ((size_t)2 * m * 4 + 15) / 16 * 16);
+    float4 *sGuard = reinterpret_cast<float4 *>(smem_raw + L::oG);
+    TcSmemHdr *H = reinterpret_cast<TcSmemHdr *>(smem_raw + L::oG + (size_t)m * 16);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // The walk's constants are computed inside each role's region, from an opaque zero: a value
@@ -306,7 +318,22 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         p_end = (int)(npairs * (blockIdx.x + z + 1) / gridDim.x);
     };
 
-    for (int i = threadIdx.x; i < 2 * m; i += kThreads) sGuard[i] = guard[i];
+    // per subspace, in the scaled units of the fp16 operands (x' = s x, c' = s c, scores x s^2, s a
+    // power of two from the image): W = G0 + ||x|| G1 bounds |b'| + ||x'|| ||c'|| plus, over E, the
+    // absolute errors the relative model does not cover: fp16 operands below the normal range
+    // (<= 2^-25 per element of x', of c' and of the bias) and the oracle's own float32 chain when
+    // its terms are subnormal (<= 2^-150 per operation, times s^2)
+    {
+        const float *scales = reinterpret_cast<const float *>(img + (size_t)m * S::kBBytes);
+        constexpr float kRootSub = SUB == 8 ? 2.8284271f : 2.0f;
+        constexpr float kappa = 2.9802322e-8f * kRootSub / tc_error_constant(SUB);  // 2^-25 sqrt(sub) / E
+        for (int i = threadIdx.x; i < m; i += kThreads) {
+            const float sc = scales[i], g0 = guard[2 * i], g1 = guard[2 * i + 1];
+            const float tiny = sc * 2.6469779601696886e-23f;  // s 2^-75
+            sGuard[i] = make_float4(g0 * sc * sc + kappa * (g1 * sc + 1.0f / kRootSub) + (SUB + 1) * tiny * tiny / tc_error_constant(SUB),
+                                    (g1 * sc + kappa) * sc, sc, 1.0f / (sc * sc));
+        }
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&H->b_full[i], 1);
@@ -378,7 +405,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 #ifdef CSPQ_TC_PROBES
                                 if ((probe & 256) && s >= S::kSteps / 2) break;  // (timing probe: half the MMAs)
 #endif
-                                if (!(probe & 2)) mma_tf32(tacc + c * kCW, da[s], db[c][s], s > 0);
+                                if (!(probe & 2)) mma_f16(tacc + c * kCW, da[s], db[c][s], s > 0);
                             }
                             mma_commit(tfull + c);  // the last one also frees A stage `as`
                         }
@@ -435,7 +462,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         const int q = warp & 3;
         const int r = 32 * q + lane;
         constexpr float kE = tc_error_constant(SUB);
-        static_assert(S::kSteps == (SUB == 8 ? 4 : 2), "tc_error_constant counts K = 8 MMA steps");
+        static_assert(S::kSteps == (SUB == 8 ? 2 : 1), "tc_error_constant budgets two K = 8 steps per K = 16 MMA");
         // the group's x ring: owned item k (item e + kGroups k) lives in slot k % kRing
         static_assert(kRing == kPD + 1, "slot rotation below assumes kRing == kPD + 1");
         auto ring = [&](int slot) -> unsigned char * {
@@ -462,7 +489,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         // A row of one of the group's items (A stage = item % kNA: e or e + kGroups) from
         // the staged x of ring slot `slot`; returns ||x|| rounded up
         static_assert(kNA == 2 * kGroups, "A stage = item % kNA: the group's items alternate between e and e + kGroups");
-        auto convert = [&](int slot, int stage) -> float {
+        auto convert = [&](int slot, int stage, int jsub) -> float {
             const TIn *xr = reinterpret_cast<const TIn *>(ring(slot));
             float x[SUB];
             if constexpr (sizeof(TIn) == 4) {
@@ -475,35 +502,33 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 #pragma unroll
                 for (int tt = 0; tt < SUB; ++tt) x[tt] = (float)xr[tt];
             }
-            // Veltkamp split on the FMA pipe (the ALU pipe bounds the epilogue):
-            // xh = x rounded to 11 significant bits (exactly tf32), xl = x - xh exactly;
-            // the MMA reads xl truncated to tf32 (<= 2^-10 |xl| <= 2^-21 |x|).
-            float xh[SUB], xl[SUB], ss = 0.f;
+            // fp16 split of the scaled row x' = s x (s: the subspace's power of two, so x' is exact):
+            // xh = x' rounded to fp16, xl = (x' - xh) rounded to fp16 -- x' - xh is exact in fp32 and
+            // |x' - xh - xl| <= 2^-22 |x'| (2^-25 absolute below the fp16 normal range).  Bytes
+            // times a power of two are exact in fp16: no low part.
+            const float sc = sGuard[jsub].z;
+            uint32_t h[SUB / 2], l[SUB / 2];
+            float ss = 0.f;
 #pragma unroll
-            for (int tt = 0; tt < SUB; ++tt) {
-                if constexpr (sizeof(TIn) == 1) {  // bytes are exact in tf32: no split
-                    xh[tt] = x[tt];
-                    xl[tt] = 0.f;
-                } else {
-                    const float c = __fmul_rn(x[tt], 8193.0f);
-                    xh[tt] = __fsub_rn(c, __fsub_rn(c, x[tt]));
-                    xl[tt] = __fsub_rn(x[tt], xh[tt]);
-                }
-                ss = __fmaf_rn(x[tt], x[tt], ss);
+            for (int pp = 0; pp < SUB / 2; ++pp) {
+                const float a = __fmul_rn(x[2 * pp], sc), b = __fmul_rn(x[2 * pp + 1], sc);
+                h[pp] = pack_f16x2(a, b);
+                if constexpr (sizeof(TIn) == 1) l[pp] = 0u;
+                else l[pp] = pack_f16x2(__fsub_rn(a, f16_lo(h[pp])), __fsub_rn(b, f16_hi(h[pp])));
+                ss = __fmaf_rn(x[2 * pp], x[2 * pp], ss);
+                ss = __fmaf_rn(x[2 * pp + 1], x[2 * pp + 1], ss);
             }
             if (!(probe & 4)) {
                 unsigned char *rowp = sA + stage * S::kABytes + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16;
-                auto st = [&](int c, float a0, float a1, float a2, float a3) {
-                    *reinterpret_cast<float4 *>(rowp + c * 128) = make_float4(a0, a1, a2, a3);
+                auto st = [&](int c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+                    *reinterpret_cast<uint4 *>(rowp + c * 128) = make_uint4(a0, a1, a2, a3);
                 };
+                constexpr uint32_t kOnes = 0x3C003C00u;  // (1.0, 1.0): the two bias parts
                 if constexpr (SUB == 8) {
-                    st(0, xh[0], xh[1], xh[2], xh[3]); st(1, xh[4], xh[5], xh[6], xh[7]);
-                    st(2, xh[0], xh[1], xh[2], xh[3]); st(3, xh[4], xh[5], xh[6], xh[7]);
-                    st(4, xl[0], xl[1], xl[2], xl[3]); st(5, xl[4], xl[5], xl[6], xl[7]);
-                    st(6, 1.f, 1.f, 0.f, 0.f); st(7, 0.f, 0.f, 0.f, 0.f);
+                    st(0, h[0], h[1], h[2], h[3]); st(1, h[0], h[1], h[2], h[3]);
+                    st(2, l[0], l[1], l[2], l[3]); st(3, kOnes, 0u, 0u, 0u);
                 } else {
-                    st(0, xh[0], xh[1], xh[2], xh[3]); st(1, xh[0], xh[1], xh[2], xh[3]);
-                    st(2, xl[0], xl[1], xl[2], xl[3]); st(3, 1.f, 1.f, 0.f, 0.f);
+                    st(0, h[0], h[1], h[0], h[1]); st(1, l[0], l[1], kOnes, 0u);
                 }
             }
             fence_proxy_async();
@@ -527,7 +552,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         ItemIter ip = ii;
         for (int d = 0; d < kPD; ++d, ip.advance(kGroups)) prefetch(ip, d);
         float norm_cur = 0.f;
-        if (ii.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(0, e); }
+        if (ii.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(0, e, ii.j); }
         ItemIter ic = ii;
         ic.advance(kGroups);
         uint32_t rel = 0;  // pairs below rel are released by this thread
@@ -550,7 +575,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             float norm_next = 0.f;
             if (ic.valid()) {
                 if (!(probe & 32)) cp_async_wait<kPD - 1>();
-                norm_next = convert(s_next, (int)((it + kGroups) % kNA));
+                norm_next = convert(s_next, (int)((it + kGroups) % kNA), ic.j);
             }
             const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
@@ -634,7 +659,12 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             // (An indicator < 2^-24 can vanish in a sum; its value is > 3.9 E W from m1, outside
             // the 2 E W that exactness needs.)
             const float m1 = fmin3(fmin3(cls[0], cls[1], cls[2]), fmin3(cls[3], cls[4], cls[5]), fmin3(cls[6], cls[7], cls[8]));
-            const float W = sGuard[2 * j] + xnorm * sGuard[2 * j + 1];
+            const float4 gj = sGuard[j];  // (G0, G1, s, 1 / s^2)
+            float W = gj.x + xnorm * gj.y;
+            // The scaled scores have more range than the oracle's float32 chain: when its terms can
+            // reach 2^127 in the original units (W / s^2) the oracle may overflow to inf / NaN where
+            // the tensor score is finite -- W becomes NaN (inf x 0) and the row is flagged
+            W = __fmaf_rn(__fmul_rn(W, 2.0f * gj.w), 0.0f, W);
             // binary band indicator on the FMA pipe: ind(v) = sat((thr - v) 2^126), thr = m1 + 4 E W;
             // the difference is flushed to zero below 2^-126, so ind is exactly 1 (v < thr) or 0
             // (v >= thr, NaN, or W = 0 / non-finite).  One exact integer accumulator counts and
@@ -708,7 +738,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             if (row < n) {
                 if (!(probe & 64)) codes[row * cs + j * cjs] = (uint8_t)code;
                 if constexpr (kBest) {
-                    if (best_out) best_out[row * m + j] = m1;  // (a stamp run borrows best_out: nullptr then)
+                    if (best_out) best_out[row * m + j] = m1 * gj.w;  // back from the scaled units (exact: a power of two)  // (a stamp run borrows best_out: nullptr then)
                 }
             }
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 7] = clock64();
@@ -724,37 +754,70 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
     }
 }
 
-// Codebook image: per subspace, 256 rows (centroids) x K tf32 in the K-major
-// no-swizzle core-matrix layout the MMA reads.
+// Codebook image: per subspace, 256 rows (centroids) x K fp16 in the K-major no-swizzle core-matrix
+// layout the MMA reads, [-ch | -cl | -ch | bh bl 0..] of the scaled codebook c' = s c, b' = s^2 b
+// (ch = c' rounded to fp16, cl = (c' - ch) rounded to fp16), followed by the m scales.  s is the
+// power of two that puts the largest centroid norm in [32, 64) -- |c'| < 64 and b' = ||c'||^2 / 2 <
+// 2^11 are inside the fp16 range with their low parts normal, and a row overflows fp16 (-> NaN
+// scores -> flagged -> exact path) only when an |x_t| exceeds ~1000 times that norm -- lowered
+// when a caller's bias is larger than that (s^2 max|b| <= 2^15).
 template <int SUB>
 __global__ void tc_image_kernel(const float *__restrict__ CB, const float *__restrict__ B, int m,
                                 uint8_t *__restrict__ img) {
     using S = TcShape<SUB>;
     const int j = blockIdx.x, l = threadIdx.x;  // 256 threads
     const float *c = CB + ((int64_t)j * kN + l) * SUB;
-    float v[S::K];
-#pragma unroll
-    for (int k = 0; k < S::K; ++k) v[k] = 0.f;
-    float ch[SUB], cl[SUB];
+    float cv[SUB], nn = 0.f;
 #pragma unroll
     for (int t = 0; t < SUB; ++t) {
-        ch[t] = tf32_rna(c[t]);
-        cl[t] = tf32_rna(c[t] - ch[t]);
+        cv[t] = c[t];
+        nn = __fmaf_ru(cv[t], cv[t], nn);
     }
     const float b = B[(int64_t)j * kN + l];
-    const float bh = tf32_rna(b), bl = tf32_rna(b - bh);
+    __shared__ float red[2][kN / 32];
+    __shared__ float s_scale;
+    float vn = __fsqrt_ru(nn), vb = fabsf(b);
+    if (!(vn <= 3.0e38f)) vn = 0.f;  // (non-finite centroids: the scale ignores them; their scores flag)
+    if (!(vb <= 3.0e38f)) vb = 0.f;
 #pragma unroll
-    for (int t = 0; t < SUB; ++t) {
-        v[t] = -ch[t];
-        v[SUB + t] = -cl[t];
-        v[2 * SUB + t] = -ch[t];
+    for (int off = 16; off > 0; off >>= 1) {
+        vn = fmaxf(vn, __shfl_xor_sync(0xffffffffu, vn, off));
+        vb = fmaxf(vb, __shfl_xor_sync(0xffffffffu, vb, off));
     }
-    v[3 * SUB] = bh;
-    v[3 * SUB + 1] = bl;
-    unsigned char *rowp = img + (int64_t)j * S::kBBytes + (l >> 3) * S::kRowGroupBytes + (l & 7) * 16;
+    if ((l & 31) == 0) { red[0][l >> 5] = vn; red[1][l >> 5] = vb; }
+    __syncthreads();
+    if (l == 0) {
+        float mn = 0.f, mb = 0.f;
+        for (int w = 0; w < kN / 32; ++w) { mn = fmaxf(mn, red[0][w]); mb = fmaxf(mb, red[1][w]); }
+        int e = 0;
+        if (mn > 0.f) { int q; frexpf(mn, &q); e = 6 - q; }           // mn 2^e in [32, 64)
+        if (mb > 0.f) { int q; frexpf(mb, &q); e = min(e, (15 - q) / 2 - ((15 - q) < 0 && ((15 - q) & 1) ? 1 : 0)); }  // mb 2^(2e) < 2^15
+        e = max(-62, min(62, e));  // (s^2 and 1 / s^2 stay finite)
+        s_scale = ldexpf(1.0f, e);
+        reinterpret_cast<float *>(img + (size_t)m * S::kBBytes)[j] = s_scale;
+    }
+    __syncthreads();
+    const float sc = s_scale;
+    uint32_t hw[SUB / 2], lw[SUB / 2];
 #pragma unroll
-    for (int cch = 0; cch < S::kChunks; ++cch)
-        *reinterpret_cast<float4 *>(rowp + cch * 128) = make_float4(v[4 * cch], v[4 * cch + 1], v[4 * cch + 2], v[4 * cch + 3]);
+    for (int pp = 0; pp < SUB / 2; ++pp) {
+        const float a0 = -cv[2 * pp] * sc, a1 = -cv[2 * pp + 1] * sc;  // (exact: a power of two)
+        hw[pp] = pack_f16x2(a0, a1);
+        lw[pp] = pack_f16x2(a0 - f16_lo(hw[pp]), a1 - f16_hi(hw[pp]));
+    }
+    const float bs = b * sc * sc;
+    const uint32_t bw = pack_f16x2(bs, 0.f);
+    const uint32_t bias = pack_f16x2(f16_lo(bw), bs - f16_lo(bw));  // (bh, bl)
+    unsigned char *rowp = img + (int64_t)j * S::kBBytes + (l >> 3) * S::kRowGroupBytes + (l & 7) * 16;
+    auto st = [&](int cch, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
+        *reinterpret_cast<uint4 *>(rowp + cch * 128) = make_uint4(a0, a1, a2, a3);
+    };
+    if constexpr (SUB == 8) {
+        st(0, hw[0], hw[1], hw[2], hw[3]); st(1, lw[0], lw[1], lw[2], lw[3]);
+        st(2, hw[0], hw[1], hw[2], hw[3]); st(3, bias, 0u, 0u, 0u);
+    } else {
+        st(0, hw[0], hw[1], lw[0], lw[1]); st(1, hw[0], hw[1], bias, 0u);
+    }
 }
 
 template <int SUB, typename TIn>
@@ -808,7 +871,7 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const flo
 
 size_t encode_tc_image_bytes(int m, int k, int sub) {
     if (k != kN || (sub != 4 && sub != 8)) return 0;
-    return (size_t)m * (sub == 8 ? TcShape<8>::kBBytes : TcShape<4>::kBBytes);
+    return (size_t)m * (sub == 8 ? TcShape<8>::kBBytes : TcShape<4>::kBBytes) + ((size_t)m * 4 + 15) / 16 * 16;  // + the scales
 }
 
 int encode_tc_prepare(const float *CB, const float *B, int m, int k, int sub, void *img, cudaStream_t st) {
@@ -855,7 +918,7 @@ int encode_tc(const void *X, int in_dtype, int64_t n, int64_t xrs, const float *
 float encode_tc_error_constant(int sub) { return tc_error_constant(sub); }
 
 int encode_tc_max_subspaces(int sub, int in_dtype) {
-    auto fit = [](size_t fixed) { return (int)((227 * 1024 - fixed - sizeof(TcSmemHdr) - 16) / 8 / 4 * 4); };
+    auto fit = [](size_t fixed) { return (int)((227 * 1024 - fixed - sizeof(TcSmemHdr) - 16) / 16 / 4 * 4); };
     if (sub == 8) return in_dtype == CSPQ_IN_U8 ? fit(TcSmem<8, uint8_t>::oG) : fit(TcSmem<8, float>::oG);
     if (sub == 4) return in_dtype == CSPQ_IN_U8 ? fit(TcSmem<4, uint8_t>::oG) : fit(TcSmem<4, float>::oG);
     return 0;

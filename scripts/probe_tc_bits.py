@@ -23,7 +23,7 @@ for pr in probes:
     P.encode_dataset_device(X, cs, plan, out=out)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 5
+    reps = int(os.environ.get("CSPQ_PROBE_REPS", "5"))
     e0.record()
     for _ in range(reps):
         P.encode_dataset_device(X, cs, plan, out=out)
