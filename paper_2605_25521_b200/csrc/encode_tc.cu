@@ -73,11 +73,19 @@ constexpr int kThreads = 128 + 128 * kGroups;  // warpgroup 0 = MMA warp, loader
                                                // registers to the epilogue (setmaxnreg kRegsLight / kRegsEpi)
 constexpr int kRegsLight = 40, kRegsEpi = 152;  // 128 x 40 + 384 x 152 = 63,488 <= 65,536
 static_assert(128 * kRegsLight + 128 * kGroups * kRegsEpi <= 65536, "register pool");
-constexpr int kNC = 1;        // accumulator chunks per item (N = 256 / kNC per MMA, own commit + barriers):
-                              // MMA and scan overlap chunk by chunk; measured on c3: 1 = 2.16e8 vec/s,
-                              // 2 = 2.04e8, 4 = 1.44e8 (an N=64 MMA costs almost what an N=256 one does);
-                              // re-measured on the final kernel: 1 = 2.73e8 / c4 8.68e8, 2 = 2.61e8 / 8.35e8
-constexpr int kCW = 256 / kNC;  // chunk width in TMEM columns (a multiple of 64: one tcgen05.ld x64)
+// (Accumulator chunks -- N = 128 or 64 per MMA with per-chunk commits and barriers, so MMA and scan
+// overlap chunk by chunk -- were measured three times and never paid: c3 -4..-5 % with 2 chunks; an
+// N = 128 MMA costs what an N = 256 one does.)
+// The MMA warp waits on named barriers (bar.sync / bar.arrive, 160 = a group's 128 threads + the
+// MMA warp): a warp blocked in bar.sync issues nothing, whereas a suspended mbarrier wait returns
+// on every barrier operation of the CTA (~10 retries of ~11 instructions per wait, ncu source
+// counters) -- and the MMA warp shares its sub-partition with three epilogue warps, which makes
+// that sub-partition the slowest of the four.  The MMA completions (tcgen05.commit) and the bulk
+// copies need mbarriers; the epilogue warps keep waiting on those one by one (releasing a whole
+// group through a named barrier put its four warps in lockstep: -3 %).
+constexpr int kBarTEmpty = 1;   // + TMEM buffer
+constexpr int kBarAFull = 3;    // + A stage (6)
+constexpr int kBarThreads = 160;
 constexpr int kPD = 2;        // cp.async prefetch distance, in the group's own items
 constexpr int kRing = 3;      // x slots per group (> kPD: an item's slot outlives its fix-up)
 
@@ -137,6 +145,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         if ((++spins & 255u) == 0) t0 = mbar_wait_check(t0);
     }
 }
+__device__ __forceinline__ void bar_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kBarThreads) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(kBarThreads) : "memory"); }
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;
     asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
@@ -172,7 +182,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int n = kN) {
 __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-                 "l"(da), "l"(db), "r"(make_idesc(kCW)), "r"(accumulate) : "memory");
+                 "l"(da), "l"(db), "r"(make_idesc(kN)), "r"(accumulate) : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -219,8 +229,7 @@ __device__ __forceinline__ float exact_score(const float (&x)[SUB], const float 
 
 struct TcSmemHdr {
     uint64_t b_full[2], b_empty[2];
-    uint64_t a_full[kNA];
-    uint64_t t_full[4][kNC], t_empty[4][kNC];  // [item & 3][chunk] (TMEM buffer item & 1): never 2 phases off
+    uint64_t t_full[4];  // MMA completion of item it: [it & 3] (TMEM buffer it & 1): never 2 phases off
     uint32_t tmem_base;
 };
 
@@ -339,13 +348,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             mbar_init(&H->b_full[i], 1);
             mbar_init(&H->b_empty[i], 1 + 128 * kGroups);  // MMA commit + every epilogue thread (fix-up reads sC)
         }
-        for (int i = 0; i < 4; ++i) {
-            for (int c = 0; c < kNC; ++c) {
-                mbar_init(&H->t_full[i][c], 1);
-                mbar_init(&H->t_empty[i][c], 128);
-            }
-        }
-        for (int i = 0; i < kNA; ++i) mbar_init(&H->a_full[i], 128);
+        for (int i = 0; i < 4; ++i) mbar_init(&H->t_full[i], 1);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -369,48 +372,44 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         uint32_t it = 0, jt = 0;
         int p_begin, p_end, ntiles;
         pair_range(p_begin, p_end, ntiles);
+        // descriptors = the stage-0 / step-0 ones plus multiples of the stage and step strides in the
+        // 14-bit address field (shared memory is < 256 KB, so the sums never carry out of it)
+        const uint64_t da0 = make_desc(smem_u32(sA), 128, S::kRowGroupBytes), db0 = make_desc(smem_u32(sB), 128, S::kRowGroupBytes);
+        int as = 0;  // A stage = it % kNA
         for (int p = p_begin; p < p_end; ++p, ++jt) {
             const int g = p / m;
             const int tn = min(ntiles - g * gs, gs);
             {
                 const int jb = jt & 1;
                 mbar_wait(&H->b_full[jb], (jt >> 1) & 1);
-                for (int t = 0; t < tn; ++t, ++it) {
-                    const int as = it % kNA, tb = it & 1;
+                for (int t = 0; t < tn; ++t, ++it, as = (as == kNA - 1) ? 0 : as + 1) {
+                    const int tb = it & 1;
                     // everything the issue needs is computed before the waits: after the accumulator
                     // is handed back only the fence, the MMAs and the commit remain
-                    const uint32_t a0 = smem_u32(sA + as * S::kABytes), b0 = smem_u32(sB + jb * S::kBBytes);
-                    uint64_t da[S::kSteps], db[kNC][S::kSteps];
+                    uint64_t da[S::kSteps], db[S::kSteps];
 #pragma unroll
                     for (int s = 0; s < S::kSteps; ++s) {
-                        da[s] = make_desc(a0 + 2 * s * 128, 128, S::kRowGroupBytes);
-#pragma unroll
-                        for (int c = 0; c < kNC; ++c)  // centroids c kCW ..
-                            db[c][s] = make_desc(b0 + (uint32_t)(c * (kCW / 8) * S::kRowGroupBytes) + 2 * s * 128, 128, S::kRowGroupBytes);
+                        da[s] = da0 + (uint32_t)(as * (S::kABytes >> 4) + s * (256 >> 4));
+                        db[s] = db0 + (uint32_t)(jb * (S::kBBytes >> 4) + s * (256 >> 4));
                     }
                     const uint32_t tacc = tmem + tb * kN;
-                    uint64_t *const tfull = &H->t_full[it & 3][0], *const tempty = &H->t_empty[(it - 2) & 3][0];
-                    const uint32_t tepar = ((it - 2) >> 2) & 1;
-                    mbar_wait(&H->a_full[as], (it / kNA) & 1);
+                    uint64_t *const tfull = &H->t_full[it & 3];
+                    bar_sync(kBarAFull + as);  // the A rows of item it (its group's fence.proxy.async precedes)
                     if (stamp && lane == 0 && it < kStampItems) stamp[it * 8 + 0] = clock64();
+                    if (it >= 2) bar_sync(kBarTEmpty + tb);  // buffer tb drained by the scan of item it - 2
+                    if (stamp && lane == 0 && it < kStampItems) stamp[it * 8 + 1] = clock64();
+                    tc_fence_after();
+                    if (elect_one()) {
 #pragma unroll
-                    for (int c = 0; c < kNC; ++c) {
-                        // chunk c of buffer tb drained by the scan of item it - 2
-                        if (it >= 2) mbar_wait(tempty + c, tepar);
-                        if (stamp && lane == 0 && c == 0 && it < kStampItems) stamp[it * 8 + 1] = clock64();
-                        tc_fence_after();
-                        if (elect_one()) {
-#pragma unroll
-                            for (int s = 0; s < S::kSteps; ++s) {
+                        for (int s = 0; s < S::kSteps; ++s) {
 #ifdef CSPQ_TC_PROBES
-                                if ((probe & 256) && s >= S::kSteps / 2) break;  // (timing probe: half the MMAs)
+                            if ((probe & 256) && s >= (S::kSteps + 1) / 2) break;  // (timing probe: half the MMAs)
 #endif
-                                if (!(probe & 2)) mma_f16(tacc + c * kCW, da[s], db[c][s], s > 0);
-                            }
-                            mma_commit(tfull + c);  // the last one also frees A stage `as`
+                            if (!(probe & 2)) mma_f16(tacc, da[s], db[s], s > 0);
                         }
-                        __syncwarp();
+                        mma_commit(tfull);  // (completion also frees A stage `as`)
                     }
+                    __syncwarp();
                     if (stamp && lane == 0 && it < kStampItems) stamp[it * 8 + 2] = clock64();
                 }
                 if (elect_one()) mma_commit(&H->b_empty[jb]);
@@ -426,7 +425,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 long long t0 = clock64();
                 while (!done && clock64() - t0 < 4000000) {
                     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                                 : "=r"(done) : "r"(smem_u32(&H->t_full[it & 3][0])), "r"((it >> 2) & 1) : "memory");
+                                 : "=r"(done) : "r"(smem_u32(&H->t_full[it & 3])), "r"((it >> 2) & 1) : "memory");
                 }
                 stamp[it * 8 + 3] = clock64();
             }
@@ -532,7 +531,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 }
             }
             fence_proxy_async();
-            mbar_arrive(&H->a_full[stage]);
+            bar_arrive(kBarAFull + stage);
             return __fsqrt_ru(ss) * 1.000001f;
         };
         // b_empty[p & 1] phase p >> 1 belongs to pair p.  A group that owns no item of
@@ -591,18 +590,16 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             for (int c = 0; c < 4; ++c) scm[c] = pos_inf_f();
 #pragma unroll
             for (int ch = 0; ch < 4 && !(probe & 1); ++ch) {
-                constexpr int kLdPerChunk = kCW / 64;
-                const int c = ch / kLdPerChunk;
-                if (ch % kLdPerChunk == 0) {
-                    mbar_wait(&H->t_full[it & 3][c], (it >> 2) & 1);
-                    if (stamp && r == 0 && ch == 0 && it < kStampItems) stamp[it * 8 + 5] = clock64();
+                if (ch == 0) {
+                    mbar_wait(&H->t_full[it & 3], (it >> 2) & 1);
+                    if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 5] = clock64();
                     tc_fence_after();
                 }
                 uint32_t v[64];
                 tmem_ld64(tmem + ((uint32_t)(32 * q) << 16) + tb * kN + ch * 64, v);
-                if (ch % kLdPerChunk == kLdPerChunk - 1) {  // chunk c is in registers: hand it back
+                if (ch == 3) {  // the whole accumulator is in registers or reduced: hand the buffer back
                     tc_fence_before();
-                    mbar_arrive(&H->t_empty[it & 3][c]);
+                    bar_arrive(kBarTEmpty + tb);
                     if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 4] = clock64();
                 }
 #define SV(i) __uint_as_float(v[(i)])
@@ -635,10 +632,8 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 #undef SV
             }
             if (probe & 1) {  // (timing probe: no TMEM reads; still walk the barriers)
-                for (int c = 0; c < kNC; ++c) {
-                    mbar_wait(&H->t_full[it & 3][c], (it >> 2) & 1);
-                    mbar_arrive(&H->t_empty[it & 3][c]);
-                }
+                mbar_wait(&H->t_full[it & 3], (it >> 2) & 1);
+                bar_arrive(kBarTEmpty + tb);
             }
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 6] = clock64();
             const float xnorm = norm_cur;
