@@ -118,8 +118,9 @@ int cspq_encode_with_scores(const void *X, int32_t in_dtype, int64_t n, int32_t 
                             const float *CB, const float *B, int32_t m, int32_t k, int32_t sub,
                             int32_t *codes, float *best, int32_t variant, void *stream);
 
-/* Tensor-core encode (tcgen05.mma kind::tf32, sm_100a): the same codes as
- * cspq_encode -- the oracle's, bit for bit -- computed as a 3xTF32 GEMM with
+/* Tensor-core encode (tcgen05.mma kind::f16 on fp16 hi/lo splits of the
+ * power-of-two scaled rows and codebook, fp32 accumulation, sm_100a): the same
+ * codes as cspq_encode -- the oracle's, bit for bit -- computed as a GEMM with
  * the bias folded in, an exact argmin/runner-up epilogue on the TMEM
  * accumulators and an exact fix-up of every subvector whose runner-up lies
  * within the tensor-core error band.  Needs k == 256, sub in {4, 8},

@@ -3,12 +3,17 @@
 // Same contract as encode.cu (the oracle's codes bit for bit; reference:
 // /root/reference/pkg/src/cspq/kernels.py:108-316), different engine:
 //
-//   scores  S = A . B^T  on tcgen05.mma.kind::tf32 (3xTF32 split, bias folded):
-//     A row (one x subvector)  = [ xh | xh | xl | 1 1 0.. ]           (tf32)
-//     B row (one centroid)     = [-ch |-cl |-ch | bh bl 0.. ]          (tf32)
-//     => S[i][l] = bh + bl - (xh.ch + xh.cl + xl.ch) ~= b_l - x_i.c_l
-//     x = xh + xl, c = ch + cl, b = bh + bl with round-to-nearest tf32 parts.
-//     For uint8 rows xh = x exactly and xl = 0.
+//   scores  S = A . B^T  on tcgen05.mma.kind::f16 (fp16 hi/lo split, fp32 accumulation, bias folded):
+//     A row (one x subvector)  = [ xh | xh | xl | 1 1 0.. ]           (fp16)
+//     B row (one centroid)     = [-ch |-cl |-ch | bh bl 0.. ]          (fp16)
+//     => S[i][l] = bh + bl - (xh.ch + xh.cl + xl.ch) ~= s^2 (b_l - x_i.c_l)
+//     of the scaled operands x' = s x, c' = s c, b' = s^2 b: s is the subspace's power of two that
+//     puts the largest centroid norm in [32, 64) (tc_image_kernel), so every part sits inside the
+//     fp16 range; x' = xh + xl, c' = ch + cl, b' = bh + bl with round-to-nearest fp16 parts
+//     (22 significant bits, as the 3xTF32 split this replaced).  For uint8 rows xl = 0.
+//     K = 32 (d_sub 8) is two K = 16 MMAs per item, K = 16 (d_sub 4) one -- half the tensor work of
+//     the tf32 form.  c3 runs into the 1,000 W power cap: with half the MMAs the SM clock under the
+//     cap rises from ~1,690 to ~1,880 MHz (bench c3 +13 % together with the shorter MMA chain).
 //   accumulators in TMEM (128 lanes = rows x 256 columns = centroids), two
 //   buffers so the MMA of tile t+1 overlaps the epilogue of tile t;
 //   epilogue warps read their rows with tcgen05.ld (64 columns per load) and
@@ -18,35 +23,49 @@
 //   nine "class" minima (position inside the block) catch a runner-up that
 //   shares the winner's block, because a block and a class intersect in at
 //   most one centroid.  Block slot s starts at centroid 8s - (s & 1); the
-//   code is that start + class.
+//   code is that start + class.  The 32 block minima are folded, chunk by chunk, into 8
+//   "super-block" and 4 "super-class" minima (the same two-partition argument one level up), so the
+//   selection looks at 9 + 8 + 4 = 21 candidates.
 //   A (row, subspace) whose runner-up lies within the error band of the
 //   tensor-core score is re-encoded exactly by its warp (strict fp32 chains,
 //   warp-shuffle argmin) -- the same fix-up as the SIMT kernel.
 //
-//   Error band (per score, |S_tc - s_oracle| <= E):
-//     tf32 splitting of x, c, b:   4 * 2^-22 (|b| + sum|x_t c_t|)  (x's low part
-//                                  is truncated by the MMA: 2^-21 |x|)
-//     tensor-core accumulation:    2^-22 per K=8 MMA step (products of tf32
-//                                  operands are exact in fp32; each step is
-//                                  modelled as <= 2 roundings of 2^-23 of the
-//                                  running magnitude) -> 4 * 2^-22 for K = 32
+//   Error band (per score, in the scaled units, |S_tc - s^2 s_oracle| <= E W + absolute terms):
+//     fp16 splitting of x', c', b': 4 * 2^-22 (|b'| + sum|x'_t c'_t|)  (three parts of 2^-22 and
+//                                  the dropped xl.cl)
+//     tensor-core accumulation:    2^-22 per 8 products (products of fp16 operands are exact in
+//                                  fp32; 8 products + the running sum are modelled as <= 2
+//                                  roundings of 2^-23 of the running magnitude) -> 4 * 2^-22 for
+//                                  K = 32
 //     the oracle's own rounding:   (sub+1) 2^-24 (|b| + sum|x_t c_t|)
+//     absolute terms:              2^-25 per element of x', c' and the bias whose fp16 parts fall
+//                                  below the normal range, and 2^-150 s^2 per operation of the
+//                                  oracle's chain when its float32 terms are subnormal
 //   The accumulation term is a model of undocumented hardware; measured
-//   errors (scripts/tc_error.py, tests/test_encode_tc_gpu.py) stay >= 6x
-//   below the resulting E on every data regime tried.
+//   errors (scripts/tc_error.py, tests/test_encode_tc_gpu.py) stay >= 7x
+//   below the resulting E on every data regime tried (max 2.8e-7 W vs E = 2.2e-6 W).
 //   with sum|x_t c_t| <= ||x|| max_l ||c_l||; a runner-up within 4E (x2
-//   safety) of the best is flagged.
+//   safety) of the best is flagged.  Rows beyond the fp16 range of their subspace (|x_t| more than
+//   ~1000 x the largest centroid norm) give NaN scores and are flagged; rows whose oracle chain can
+//   overflow float32 (W / s^2 >= 2^127) are flagged too -- the scaled scores have more range.
 //
-// Warp roles (64 + 128 kGroups threads, one CTA per SM, persistent over a contiguous range of
-// (row group, subspace) pairs):
-//   warp 0      TMEM allocation + MMA issue (the warp walks the items, one elected lane issues)
-//   warp 1      bulk copies of the prepared codebook image + fp32 codebook (cp.async.bulk)
-//   warps 2..   kGroups epilogue groups of 4 warps (TMEM lane quadrant = warp % 4); item it
-//               belongs to group it % kGroups and TMEM buffer it & 1.  A group drains its
-//               item's accumulator (block + class minima), writes the A operand of its next
-//               item (x prefetched with cp.async, tf32 split), selects the winner with the
-//               band indicators (runner-up within the error band => flag), applies the exact
-//               fix-up (or, in mark mode, flags the pair for the caller), stores codes.
+// Warp roles (128 + 128 kGroups threads, one CTA per SM, persistent over a contiguous range of
+// (row group, subspace) pairs).  The kernel is bound by issue slots: on this SM a half-rate
+// ALU-pipe instruction (FMNMX3: 276 of ~710 instructions per warp-item) holds a sub-partition's issue
+// port for two cycles (scripts/micro/issue_mix.cu), so time ~ 2 x ALU + other instructions.
+//   warps 0-3   one warpgroup that hands its registers to the others (setmaxnreg 40 / 152):
+//     warp 0    TMEM allocation + MMA issue (the warp walks the items, one elected lane issues);
+//               waits for A rows and drained accumulators on named barriers (bar.sync: no retries)
+//     warp 1    bulk copies of the prepared codebook image + fp32 codebook (cp.async.bulk)
+//     warps 2-3 idle
+//   warps 4..   kGroups epilogue groups of 4 warps (TMEM lane quadrant = warp % 4); item it
+//               belongs to group it % kGroups and TMEM buffer it & 1.  A group writes the A rows of
+//               its next item (x prefetched with cp.async, scaled, fp16 split) into its other A
+//               stage, drains its item's accumulator (block, class, super-block and super-class
+//               minima, all in registers), selects the winner with binary band indicators summed
+//               into one exact integer accumulator (runner-up within the error band => flag),
+//               applies the exact fix-up (or, in mark mode, flags the pair for the caller), stores
+//               codes.
 
 #include <atomic>
 #include <cstdlib>
