@@ -152,7 +152,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     // suspend (woken by the phase flip) instead of busy polling: spinning warps steal issue slots
     // from the epilogue warps that share their SM sub-partition.  A suspended try_wait also
     // returns on other barrier traffic of the CTA (~5 times per wait, ncu source counters), so the
-    // retry path is kept to the try itself plus a counter: the clock is read every 256th retry
+    // retry path is kept to the try itself plus a counter: the clock is read every 256th retry.
+    // (Four tries and a branch each inside one asm block -- 4 instead of 11 instructions per retry --
+    // ran 2 % SLOWER on c3 and c4: the shorter loop simply polls more often; the wait is time, not
+    // instructions.)
     const uint32_t addr = smem_u32(bar);
     uint32_t spins = 0;
     long long t0 = 0;
@@ -238,6 +241,19 @@ __device__ __forceinline__ float f16_hi(uint32_t v) {
     return f;
 }
 
+// a - (one fp16 half of v) in one mixed-precision add (SASS FHADD; exact: the half is a's own
+// rounding, so the difference has <= 13 significant bits) instead of a conversion and a subtraction
+__device__ __forceinline__ float f16_resid_lo(uint32_t v, float a) {
+    float d;
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tneg.f16 l, l;\n\tadd.rn.f32.f16 %0, l, %2;\n\t}" : "=f"(d) : "r"(v), "f"(a));
+    return d;
+}
+__device__ __forceinline__ float f16_resid_hi(uint32_t v, float a) {
+    float d;
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tneg.f16 h, h;\n\tadd.rn.f32.f16 %0, h, %2;\n\t}" : "=f"(d) : "r"(v), "f"(a));
+    return d;
+}
+
 template <int SUB>
 __device__ __forceinline__ float exact_score(const float (&x)[SUB], const float *c, float b) {
     float dd = __fmul_rn(x[0], c[0]);
@@ -264,6 +280,7 @@ struct ItemIter {
     }
     __device__ bool valid() const { return p < p_end; }
     __device__ int64_t tile() const { return (int64_t)g * gs + t; }
+    __device__ int tile32() const { return valid() ? g * gs + t : -1; }  // (ntiles < 2^31: checked by the launch)
     // k items ahead (jt counts every pair boundary crossed, as k single steps would)
     __device__ void advance(int k) {
         t += k;
@@ -486,10 +503,20 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         auto ring = [&](int slot) -> unsigned char * {
             return sX + ((size_t)e * kRing + slot) * L::kXBytes + r * SUB * sizeof(TIn);
         };
-        auto prefetch = [&](const ItemIter &pi, int slot) {
-            const int64_t row = pi.tile() * kTM + r;
-            const bool ok = pi.valid() && row < n;
-            const TIn *src = X + (ok ? row * xs + (int64_t)pi.j * xjs : 0);
+        // One item of the walk as the loop needs it: tile index (-1 past the end), subspace, pair
+        // counter.  The loop keeps the current item, the next one (A conversion) and a running
+        // iterator two items ahead (x prefetch): one ItemIter::advance per iteration instead of three.
+        struct ItemRef { int tile, j; uint32_t jt; };
+        auto ref_of = [](const ItemIter &w) { return ItemRef{w.tile32(), w.j, w.jt}; };
+        // row addresses from per-thread bases: row r of tile t, subspace j sits at
+        // xrow + t (128 xs) + j xjs -- two wide multiply-adds instead of the 64-bit row * stride chain
+        // (prefetch + code store took 79 of ~710 instructions per warp-item); row < n is t < tlim
+        const TIn *const xrow = X + (int64_t)r * xs;
+        const int64_t xs_tile = xs * kTM;
+        const uint32_t tlim = n > r ? (uint32_t)((n - r + kTM - 1) / kTM) : 0u;
+        auto prefetch = [&](const ItemRef &pi, int slot) {
+            const bool ok = (uint32_t)pi.tile < tlim;
+            const TIn *src = ok ? xrow + ((int64_t)pi.tile * xs_tile + (int64_t)pi.j * xjs) : X;
             unsigned char *dst = ring(slot);
             constexpr int bytes = SUB * (int)sizeof(TIn);
             if constexpr (bytes == 32) {
@@ -526,13 +553,13 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             // times a power of two are exact in fp16: no low part.
             const float sc = sGuard[jsub].z;
             uint32_t h[SUB / 2], l[SUB / 2];
-            float ss = 0.f;
+            float ss = 7.8886090522101181e-31f;  // 2^-100: never subnormal (the approximate sqrt below flushes)
 #pragma unroll
             for (int pp = 0; pp < SUB / 2; ++pp) {
                 const float a = __fmul_rn(x[2 * pp], sc), b = __fmul_rn(x[2 * pp + 1], sc);
                 h[pp] = pack_f16x2(a, b);
                 if constexpr (sizeof(TIn) == 1) l[pp] = 0u;
-                else l[pp] = pack_f16x2(__fsub_rn(a, f16_lo(h[pp])), __fsub_rn(b, f16_hi(h[pp])));
+                else l[pp] = pack_f16x2(f16_resid_lo(h[pp], a), f16_resid_hi(h[pp], b));
                 ss = __fmaf_rn(x[2 * pp], x[2 * pp], ss);
                 ss = __fmaf_rn(x[2 * pp + 1], x[2 * pp + 1], ss);
             }
@@ -551,7 +578,12 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             }
             fence_proxy_async();
             bar_arrive(kBarAFull + stage);
-            return __fsqrt_ru(ss) * 1.000001f;
+            // ||x|| rounded up: the sum's roundings (<= sub 2^-24 relative, all terms positive), the
+            // approximate square root (<= 2^-22) and the product's rounding stay below the factor's
+            // 8 ulp; the 2^-100 floor adds 2^-50 at most (a wider band, never a narrower one)
+            float sq;
+            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(ss));
+            return sq * 1.000001f;
         };
         // b_empty[p & 1] phase p >> 1 belongs to pair p.  A group that owns no item of
         // a pair reaches the next pair early; its arrival must not land in the still
@@ -565,14 +597,17 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         // and kGroups kPD items ahead for the A conversion and the x prefetch.
         int p_begin, p_end, ntiles;
         pair_range(p_begin, p_end, ntiles);
-        ItemIter ii(p_begin, p_end, m, gs, ntiles);
-        ii.advance(e);
-        ItemIter ip = ii;
-        for (int d = 0; d < kPD; ++d, ip.advance(kGroups)) prefetch(ip, d);
+        ItemIter ip(p_begin, p_end, m, gs, ntiles);
+        ip.advance(e);
+        ItemRef ii = ref_of(ip);  // the current item
+        prefetch(ii, 0);
+        ip.advance(kGroups);
+        ItemRef ic = ref_of(ip);  // the group's next item (A conversion)
+        static_assert(kPD == 2, "two items prefetched ahead of the loop");
+        prefetch(ic, 1);
+        ip.advance(kGroups);      // ip: the item whose x the iteration prefetches
         float norm_cur = 0.f;
-        if (ii.valid()) { cp_async_wait<kPD - 1>(); norm_cur = convert(0, e, ii.j); }
-        ItemIter ic = ii;
-        ic.advance(kGroups);
+        if (ii.tile >= 0) { cp_async_wait<kPD - 1>(); norm_cur = convert(0, e, ii.j); }
         uint32_t rel = 0;  // pairs below rel are released by this thread
         // ring slots of the current item, the next one (A conversion) and the prefetched one
         int s_cur = 0, s_next = 1, s_pf = 2;
@@ -582,18 +617,21 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             s_next = s_pf;
             s_pf = s_old;
         };
+        int st_next = e + kGroups;  // A stage of the next item: the group's items alternate between e and e + kGroups
+        uint8_t *const crow = codes + (int64_t)r * cs;
+        const int64_t cs_tile = cs * kTM;
 
-        for (uint32_t it = e; ii.valid(); it += kGroups, ii.advance(kGroups), ic.advance(kGroups), ip.advance(kGroups),
-                                          rotate()) {
+        for (uint32_t it = e; ii.tile >= 0; it += kGroups, ii = ic, ic = ref_of(ip), ip.advance(kGroups), rotate(),
+                                            st_next = 2 * e + kGroups - st_next) {
             for (; rel < ii.jt; ++rel) release_pair(rel);  // done with those pairs' sC
             // the group's next item first: stage the x prefetch of the one after it and write its A
             // rows into the group's other A stage (free since item it - kGroups was scanned), so
             // its MMA can start as soon as a TMEM buffer is handed back
-            if (!(probe & 32)) prefetch(ip, s_pf);  // (an empty group keeps the wait count uniform)
+            if (!(probe & 32)) prefetch(ref_of(ip), s_pf);  // (an empty group keeps the wait count uniform)
             float norm_next = 0.f;
-            if (ic.valid()) {
+            if (ic.tile >= 0) {
                 if (!(probe & 32)) cp_async_wait<kPD - 1>();
-                norm_next = convert(s_next, (int)((it + kGroups) % kNA), ic.j);
+                norm_next = convert(s_next, st_next, ic.j);
             }
             const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
@@ -657,9 +695,10 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 6] = clock64();
             const float xnorm = norm_cur;
             norm_cur = norm_next;
+            const bool inb = (uint32_t)ii.tile < tlim;  // row < n
+            const int64_t coff = (int64_t)ii.tile * cs_tile + (int64_t)j * cjs;  // codes / flags offset from row r's base
             if (probe & 128) {  // (timing probe: no selection / fix-up; garbage codes)
-                const int64_t row = ii.tile() * kTM + r;
-                if (row < n && !(probe & 64)) codes[row * cs + j * cjs] = (uint8_t)(__float_as_uint(cls[0] + xnorm) & 255);
+                if (inb && !(probe & 64)) crow[coff] = (uint8_t)(__float_as_uint(cls[0] + xnorm) & 255);
                 continue;
             }
             // Final selection on the FMA pipe.  m1 = the minimum (of the class minima); the band
@@ -703,15 +742,14 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 #pragma unroll
             for (int u = 0; u < 8; ++u) tu = __fmaf_rn(ind(sbm[u]), (float)((1 << 17) + 64 * u), tu);
             const uint32_t sel = (uint32_t)(__float2int_rz(__fadd_rn(__fadd_rn(tc, ts), tu)) - kSelBase);
-            const int64_t row = ii.tile() * kTM + r;
             // block slot sb starts at column 8 sb - (sb & 1) (7-blocks at even slots, 9-blocks at odd)
             const int sb = (int)(sel >> 4) & 31;
             int code = 8 * sb - (sb & 1) + (int)(sel & 15);
-            const bool flag = (row < n) && !(sel < 512u);
+            const bool flag = inb && !(sel < 512u);
             // exact warp-cooperative re-encode of flagged rows (x and the fp32 codebook from
             // shared memory: the item's x slot stays valid until kPD more owned items)
             if constexpr (kMark) {  // mark mode (Lloyd screening): flagged rows are settled by the caller
-                if (row < n) flags[row * cs + j * cjs] = flag ? 1 : 0;
+                if (inb) (flags + (int64_t)r * cs)[coff] = flag ? 1 : 0;
                 const unsigned fm = __ballot_sync(0xffffffffu, flag);
                 if (lane == 0 && fm) atomicAdd(&g_tc_flagged, (unsigned long long)__popc(fm));
             }
@@ -749,15 +787,15 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                     if (lane == src) code = (best < pos_inf_f()) ? bl : 0;
                 }
             }
-            if (row < n) {
-                if (!(probe & 64)) codes[row * cs + j * cjs] = (uint8_t)code;
+            if (inb) {
+                if (!(probe & 64)) crow[coff] = (uint8_t)code;
                 if constexpr (kBest) {
-                    if (best_out) best_out[row * m + j] = m1 * gj.w;  // back from the scaled units (exact: a power of two)  // (a stamp run borrows best_out: nullptr then)
+                    if (best_out) best_out[((int64_t)ii.tile * kTM + r) * m + j] = m1 * gj.w;  // back from the scaled units (exact: a power of two)  // (a stamp run borrows best_out: nullptr then)
                 }
             }
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 7] = clock64();
         }
-        for (; rel < ii.jt; ++rel) release_pair(rel);  // ii.jt = every pair this CTA walked
+        for (; rel < (uint32_t)(p_end - p_begin); ++rel) release_pair(rel);  // every pair this CTA walked
         cp_async_wait<0>();
     }
     tc_fence_before();
