@@ -148,7 +148,7 @@ __device__ __noinline__ long long mbar_wait_check(long long t0) {
     if (t - t0 > 20000000000ll) __trap();
     return t0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_s(uint32_t addr, uint32_t parity) {  // addr: shared address of the mbarrier
     // suspend (woken by the phase flip) instead of busy polling: spinning warps steal issue slots
     // from the epilogue warps that share their SM sub-partition.  A suspended try_wait also
     // returns on other barrier traffic of the CTA (~5 times per wait, ncu source counters), so the
@@ -156,7 +156,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     // (Four tries and a branch each inside one asm block -- 4 instead of 11 instructions per retry --
     // ran 2 % SLOWER on c3 and c4: the shorter loop simply polls more often; the wait is time, not
     // instructions.)
-    const uint32_t addr = smem_u32(bar);
     uint32_t spins = 0;
     long long t0 = 0;
     for (;;) {
@@ -167,6 +166,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         if ((++spins & 255u) == 0) t0 = mbar_wait_check(t0);
     }
 }
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) { mbar_wait_s(smem_u32(bar), parity); }
 __device__ __forceinline__ void bar_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kBarThreads) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(kBarThreads) : "memory"); }
 __device__ __forceinline__ bool elect_one() {
@@ -252,6 +252,48 @@ __device__ __forceinline__ float f16_resid_hi(uint32_t v, float a) {
     float d;
     asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tneg.f16 h, h;\n\tadd.rn.f32.f16 %0, h, %2;\n\t}" : "=f"(d) : "r"(v), "f"(a));
     return d;
+}
+
+// Shared-memory accesses of the epilogue's hot loop by 32-bit shared address: every per-thread
+// address is computed once, made opaque (opaque32: ptxas otherwise re-derives such values from
+// %tid and the shared window base at every use -- ~80 of ~680 instructions per warp-item) and kept
+// in a register.
+__device__ __forceinline__ uint32_t opaque32(uint32_t v) { return __shfl_sync(0xffffffffu, v, threadIdx.x & 31); }
+__device__ __forceinline__ uint64_t opaque64(uint64_t v) {
+    return ((uint64_t)opaque32((uint32_t)(v >> 32)) << 32) | opaque32((uint32_t)v);
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_f(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+// cp.async of BYTES (4, 8, 16) with the ignore-src predicate: !ok writes zeros and reads nothing
+template <int BYTES>
+__device__ __forceinline__ void cp_async_pred(uint32_t dst, const void *src, bool ok) {
+    if constexpr (BYTES == 16)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %2, 0;\n\tcp.async.cg.shared.global [%0], [%1], 16, p;\n\t}" ::"r"(dst), "l"(src), "r"((uint32_t)ok));
+    else if constexpr (BYTES == 8)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %2, 0;\n\tcp.async.ca.shared.global [%0], [%1], 8, p;\n\t}" ::"r"(dst), "l"(src), "r"((uint32_t)ok));
+    else
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %2, 0;\n\tcp.async.ca.shared.global [%0], [%1], 4, p;\n\t}" ::"r"(dst), "l"(src), "r"((uint32_t)ok));
 }
 
 template <int SUB>
@@ -500,58 +542,72 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         static_assert(S::kSteps == (SUB == 8 ? 2 : 1), "tc_error_constant budgets two K = 8 steps per K = 16 MMA");
         // the group's x ring: owned item k (item e + kGroups k) lives in slot k % kRing
         static_assert(kRing == kPD + 1, "slot rotation below assumes kRing == kPD + 1");
-        auto ring = [&](int slot) -> unsigned char * {
-            return sX + ((size_t)e * kRing + slot) * L::kXBytes + r * SUB * sizeof(TIn);
-        };
+        // Per-thread constants of the loop, opaque and in registers (see opaque32): shared addresses
+        // of the thread's x ring rows and A rows, its TMEM lane, the guard table, the accumulator
+        // barriers; global row bases.  Row r of tile t, subspace j sits at xrow + t (128 xs) + j xjs
+        // -- two wide multiply-adds instead of a 64-bit row * stride chain; row < n is t < tlim.
+        const uint32_t smem0 = smem_u32(smem_raw);
+        const uint32_t sg_s = opaque32(smem0 + (uint32_t)L::oG);                                  // sGuard
+        const uint32_t tf_s = opaque32(smem0 + (uint32_t)L::oG + (uint32_t)m * 16 + (uint32_t)offsetof(TcSmemHdr, t_full));
+        const uint32_t tm_lane = opaque32(tmem + ((uint32_t)(32 * q) << 16));
+        const uint64_t xrow = opaque64((uint64_t)(uintptr_t)(X + (int64_t)r * xs));
+        const uint64_t crow = opaque64((uint64_t)(uintptr_t)(codes + (int64_t)r * cs));
+        const uint32_t tlim = opaque32(n > r ? (uint32_t)((n - r + kTM - 1) / kTM) : 0u);
+        const uint64_t xs_tile = (uint64_t)xs * (kTM * sizeof(TIn)), xjs_b = (uint64_t)xjs * sizeof(TIn);
+        const uint64_t cs_tile = (uint64_t)cs * kTM;
+        // x ring rows of the current item, the next one (A conversion) and the prefetched one: the
+        // addresses rotate, so no slot index is ever turned into an address inside the loop
+        uint32_t x_cur = opaque32(smem0 + (uint32_t)(L::oX + ((size_t)e * kRing) * L::kXBytes + r * SUB * sizeof(TIn)));
+        uint32_t x_next = x_cur + L::kXBytes, x_pf = x_cur + 2 * L::kXBytes;
+        // the thread's A row in the group's two stages (e and e + kGroups) and the stage's named
+        // barrier, packed (address | barrier << 24) so one XOR toggles both
+        static_assert(kNA == 2 * kGroups, "A stage = item % kNA: the group's items alternate between e and e + kGroups");
+        const uint32_t arow0 = smem0 + (uint32_t)(L::oA + (size_t)e * S::kABytes + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16);
+        const uint32_t apk0 = arow0 | ((uint32_t)(kBarAFull + e) << 24);
+        const uint32_t apk1 = (arow0 + kGroups * S::kABytes) | ((uint32_t)(kBarAFull + e + kGroups) << 24);
+        const uint32_t a_tog = opaque32(apk0 ^ apk1);
+        uint32_t a_next = opaque32(apk1);  // (the first item's A rows go to stage e: apk0, before the loop)
         // One item of the walk as the loop needs it: tile index (-1 past the end), subspace, pair
         // counter.  The loop keeps the current item, the next one (A conversion) and a running
         // iterator two items ahead (x prefetch): one ItemIter::advance per iteration instead of three.
         struct ItemRef { int tile, j; uint32_t jt; };
         auto ref_of = [](const ItemIter &w) { return ItemRef{w.tile32(), w.j, w.jt}; };
-        // row addresses from per-thread bases: row r of tile t, subspace j sits at
-        // xrow + t (128 xs) + j xjs -- two wide multiply-adds instead of the 64-bit row * stride chain
-        // (prefetch + code store took 79 of ~710 instructions per warp-item); row < n is t < tlim
-        const TIn *const xrow = X + (int64_t)r * xs;
-        const int64_t xs_tile = xs * kTM;
-        const uint32_t tlim = n > r ? (uint32_t)((n - r + kTM - 1) / kTM) : 0u;
-        auto prefetch = [&](const ItemRef &pi, int slot) {
+        auto prefetch = [&](const ItemRef &pi, uint32_t dst) {
             const bool ok = (uint32_t)pi.tile < tlim;
-            const TIn *src = ok ? xrow + ((int64_t)pi.tile * xs_tile + (int64_t)pi.j * xjs) : X;
-            unsigned char *dst = ring(slot);
+            // (an ignored source is never read: the address may lie outside X)
+            const unsigned char *src = reinterpret_cast<const unsigned char *>(
+                (uintptr_t)(xrow + (uint64_t)(uint32_t)pi.tile * xs_tile + (uint64_t)(uint32_t)pi.j * xjs_b));
             constexpr int bytes = SUB * (int)sizeof(TIn);
             if constexpr (bytes == 32) {
-                cp_async16(dst, src, ok ? 16 : 0);
-                cp_async16(dst + 16, reinterpret_cast<const unsigned char *>(src) + 16, ok ? 16 : 0);
-            } else if constexpr (bytes == 16) {
-                cp_async16(dst, src, ok ? 16 : 0);
-            } else if constexpr (bytes == 8) {
-                cp_async8(dst, src, ok ? 8 : 0);
+                cp_async_pred<16>(dst, src, ok);
+                cp_async_pred<16>(dst + 16, src + 16, ok);
             } else {
-                cp_async4(dst, src, ok ? 4 : 0);
+                cp_async_pred<bytes>(dst, src, ok);
             }
             cp_async_commit();
         };
-        // A row of one of the group's items (A stage = item % kNA: e or e + kGroups) from
-        // the staged x of ring slot `slot`; returns ||x|| rounded up
-        static_assert(kNA == 2 * kGroups, "A stage = item % kNA: the group's items alternate between e and e + kGroups");
-        auto convert = [&](int slot, int stage, int jsub) -> float {
-            const TIn *xr = reinterpret_cast<const TIn *>(ring(slot));
+        // A row of one of the group's items (apk: shared address of the row in the item's stage |
+        // the stage's barrier << 24) from the staged x at shared address xa; returns ||x|| rounded up
+        auto convert = [&](uint32_t xa, uint32_t apk, int jsub) -> float {
             float x[SUB];
             if constexpr (sizeof(TIn) == 4) {
 #pragma unroll
                 for (int q4 = 0; q4 < SUB / 4; ++q4) {
-                    const float4 v = reinterpret_cast<const float4 *>(xr)[q4];
+                    const float4 v = lds_f4(xa + 16 * q4);
                     x[4 * q4] = v.x; x[4 * q4 + 1] = v.y; x[4 * q4 + 2] = v.z; x[4 * q4 + 3] = v.w;
                 }
             } else {
+                uint32_t w[SUB / 4];
+                if constexpr (SUB == 8) { const uint2 v = lds_u2(xa); w[0] = v.x; w[1] = v.y; }
+                else w[0] = lds_u(xa);
 #pragma unroll
-                for (int tt = 0; tt < SUB; ++tt) x[tt] = (float)xr[tt];
+                for (int tt = 0; tt < SUB; ++tt) x[tt] = (float)((w[tt >> 2] >> (8 * (tt & 3))) & 255u);
             }
             // fp16 split of the scaled row x' = s x (s: the subspace's power of two, so x' is exact):
             // xh = x' rounded to fp16, xl = (x' - xh) rounded to fp16 -- x' - xh is exact in fp32 and
             // |x' - xh - xl| <= 2^-22 |x'| (2^-25 absolute below the fp16 normal range).  Bytes
             // times a power of two are exact in fp16: no low part.
-            const float sc = sGuard[jsub].z;
+            const float sc = lds_f(sg_s + (uint32_t)jsub * 16 + 8);  // sGuard[jsub].z
             uint32_t h[SUB / 2], l[SUB / 2];
             float ss = 7.8886090522101181e-31f;  // 2^-100: never subnormal (the approximate sqrt below flushes)
 #pragma unroll
@@ -564,20 +620,17 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 ss = __fmaf_rn(x[2 * pp + 1], x[2 * pp + 1], ss);
             }
             if (!(probe & 4)) {
-                unsigned char *rowp = sA + stage * S::kABytes + (r >> 3) * S::kRowGroupBytes + (r & 7) * 16;
-                auto st = [&](int c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3) {
-                    *reinterpret_cast<uint4 *>(rowp + c * 128) = make_uint4(a0, a1, a2, a3);
-                };
+                const uint32_t rowp = apk & 0xFFFFFFu;
                 constexpr uint32_t kOnes = 0x3C003C00u;  // (1.0, 1.0): the two bias parts
                 if constexpr (SUB == 8) {
-                    st(0, h[0], h[1], h[2], h[3]); st(1, h[0], h[1], h[2], h[3]);
-                    st(2, l[0], l[1], l[2], l[3]); st(3, kOnes, 0u, 0u, 0u);
+                    sts_u4(rowp, h[0], h[1], h[2], h[3]); sts_u4(rowp + 128, h[0], h[1], h[2], h[3]);
+                    sts_u4(rowp + 256, l[0], l[1], l[2], l[3]); sts_u4(rowp + 384, kOnes, 0u, 0u, 0u);
                 } else {
-                    st(0, h[0], h[1], h[0], h[1]); st(1, l[0], l[1], kOnes, 0u);
+                    sts_u4(rowp, h[0], h[1], h[0], h[1]); sts_u4(rowp + 128, l[0], l[1], kOnes, 0u);
                 }
             }
             fence_proxy_async();
-            bar_arrive(kBarAFull + stage);
+            bar_arrive((int)(apk >> 24));
             // ||x|| rounded up: the sum's roundings (<= sub 2^-24 relative, all terms positive), the
             // approximate square root (<= 2^-22) and the product's rounding stay below the factor's
             // 8 ulp; the 2^-100 floor adds 2^-50 at most (a wider band, never a narrower one)
@@ -600,38 +653,32 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
         ItemIter ip(p_begin, p_end, m, gs, ntiles);
         ip.advance(e);
         ItemRef ii = ref_of(ip);  // the current item
-        prefetch(ii, 0);
+        prefetch(ii, x_cur);
         ip.advance(kGroups);
         ItemRef ic = ref_of(ip);  // the group's next item (A conversion)
         static_assert(kPD == 2, "two items prefetched ahead of the loop");
-        prefetch(ic, 1);
+        prefetch(ic, x_next);
         ip.advance(kGroups);      // ip: the item whose x the iteration prefetches
         float norm_cur = 0.f;
-        if (ii.tile >= 0) { cp_async_wait<kPD - 1>(); norm_cur = convert(0, e, ii.j); }
+        if (ii.tile >= 0) { cp_async_wait<kPD - 1>(); norm_cur = convert(x_cur, apk0, ii.j); }
         uint32_t rel = 0;  // pairs below rel are released by this thread
-        // ring slots of the current item, the next one (A conversion) and the prefetched one
-        int s_cur = 0, s_next = 1, s_pf = 2;
         auto rotate = [&] {  // the current item's slot becomes the next prefetch target
-            const int s_old = s_cur;
-            s_cur = s_next;
-            s_next = s_pf;
-            s_pf = s_old;
+            const uint32_t x_old = x_cur;
+            x_cur = x_next;
+            x_next = x_pf;
+            x_pf = x_old;
         };
-        int st_next = e + kGroups;  // A stage of the next item: the group's items alternate between e and e + kGroups
-        uint8_t *const crow = codes + (int64_t)r * cs;
-        const int64_t cs_tile = cs * kTM;
 
-        for (uint32_t it = e; ii.tile >= 0; it += kGroups, ii = ic, ic = ref_of(ip), ip.advance(kGroups), rotate(),
-                                            st_next = 2 * e + kGroups - st_next) {
+        for (uint32_t it = e; ii.tile >= 0; it += kGroups, ii = ic, ic = ref_of(ip), ip.advance(kGroups), rotate(), a_next ^= a_tog) {
             for (; rel < ii.jt; ++rel) release_pair(rel);  // done with those pairs' sC
             // the group's next item first: stage the x prefetch of the one after it and write its A
             // rows into the group's other A stage (free since item it - kGroups was scanned), so
             // its MMA can start as soon as a TMEM buffer is handed back
-            if (!(probe & 32)) prefetch(ref_of(ip), s_pf);  // (an empty group keeps the wait count uniform)
+            if (!(probe & 32)) prefetch(ref_of(ip), x_pf);  // (an empty group keeps the wait count uniform)
             float norm_next = 0.f;
             if (ic.tile >= 0) {
                 if (!(probe & 32)) cp_async_wait<kPD - 1>();
-                norm_next = convert(s_next, st_next, ic.j);
+                norm_next = convert(x_next, a_next, ic.j);
             }
             const int tb = it & 1;  // TMEM buffer
             const uint32_t jt = ii.jt;
@@ -648,12 +695,12 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 #pragma unroll
             for (int ch = 0; ch < 4 && !(probe & 1); ++ch) {
                 if (ch == 0) {
-                    mbar_wait(&H->t_full[it & 3], (it >> 2) & 1);
+                    mbar_wait_s(tf_s + 8 * (it & 3), (it >> 2) & 1);
                     if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 5] = clock64();
                     tc_fence_after();
                 }
                 uint32_t v[64];
-                tmem_ld64(tmem + ((uint32_t)(32 * q) << 16) + tb * kN + ch * 64, v);
+                tmem_ld64(tm_lane + tb * kN + ch * 64, v);
                 if (ch == 3) {  // the whole accumulator is in registers or reduced: hand the buffer back
                     tc_fence_before();
                     bar_arrive(kBarTEmpty + tb);
@@ -689,16 +736,17 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 #undef SV
             }
             if (probe & 1) {  // (timing probe: no TMEM reads; still walk the barriers)
-                mbar_wait(&H->t_full[it & 3], (it >> 2) & 1);
+                mbar_wait_s(tf_s + 8 * (it & 3), (it >> 2) & 1);
                 bar_arrive(kBarTEmpty + tb);
             }
             if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 6] = clock64();
             const float xnorm = norm_cur;
             norm_cur = norm_next;
             const bool inb = (uint32_t)ii.tile < tlim;  // row < n
-            const int64_t coff = (int64_t)ii.tile * cs_tile + (int64_t)j * cjs;  // codes / flags offset from row r's base
+            uint8_t *const cptr = reinterpret_cast<uint8_t *>(  // the row's code of subspace j
+                (uintptr_t)(crow + (uint64_t)(uint32_t)ii.tile * cs_tile + (uint64_t)(uint32_t)j * (uint64_t)cjs));
             if (probe & 128) {  // (timing probe: no selection / fix-up; garbage codes)
-                if (inb && !(probe & 64)) crow[coff] = (uint8_t)(__float_as_uint(cls[0] + xnorm) & 255);
+                if (inb && !(probe & 64)) *cptr = (uint8_t)(__float_as_uint(cls[0] + xnorm) & 255);
                 continue;
             }
             // Final selection on the FMA pipe.  m1 = the minimum (of the class minima); the band
@@ -712,7 +760,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             // (An indicator < 2^-24 can vanish in a sum; its value is > 3.9 E W from m1, outside
             // the 2 E W that exactness needs.)
             const float m1 = fmin3(fmin3(cls[0], cls[1], cls[2]), fmin3(cls[3], cls[4], cls[5]), fmin3(cls[6], cls[7], cls[8]));
-            const float4 gj = sGuard[j];  // (G0, G1, s, 1 / s^2)
+            const float4 gj = lds_f4(sg_s + (uint32_t)j * 16);  // sGuard[j] = (G0, G1, s, 1 / s^2)
             float W = gj.x + xnorm * gj.y;
             // The scaled scores have more range than the oracle's float32 chain: when its terms can
             // reach 2^127 in the original units (W / s^2) the oracle may overflow to inf / NaN where
@@ -749,7 +797,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             // exact warp-cooperative re-encode of flagged rows (x and the fp32 codebook from
             // shared memory: the item's x slot stays valid until kPD more owned items)
             if constexpr (kMark) {  // mark mode (Lloyd screening): flagged rows are settled by the caller
-                if (inb) (flags + (int64_t)r * cs)[coff] = flag ? 1 : 0;
+                if (inb) cptr[flags - codes] = flag ? 1 : 0;  // (same layout as the codes)
                 const unsigned fm = __ballot_sync(0xffffffffu, flag);
                 if (lane == 0 && fm) atomicAdd(&g_tc_flagged, (unsigned long long)__popc(fm));
             }
@@ -763,8 +811,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 while (mask) {
                     const int src = __ffs(mask) - 1;
                     mask &= mask - 1;
-                    const TIn *xr = reinterpret_cast<const TIn *>(sX + ((size_t)e * kRing + s_cur) * L::kXBytes) +
-                                    (32 * q + src) * SUB;
+                    const TIn *xr = reinterpret_cast<const TIn *>(smem_raw + (x_cur - smem0)) + (src - lane) * SUB;
                     float xv[SUB];
 #pragma unroll
                     for (int tt = 0; tt < SUB; ++tt) xv[tt] = (float)xr[tt];
@@ -788,7 +835,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                 }
             }
             if (inb) {
-                if (!(probe & 64)) crow[coff] = (uint8_t)code;
+                if (!(probe & 64)) *cptr = (uint8_t)code;
                 if constexpr (kBest) {
                     if (best_out) best_out[((int64_t)ii.tile * kTM + r) * m + j] = m1 * gj.w;  // back from the scaled units (exact: a power of two)  // (a stamp run borrows best_out: nullptr then)
                 }
