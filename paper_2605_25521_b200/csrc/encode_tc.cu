@@ -82,7 +82,11 @@ constexpr int kTM = 128;     // rows per tile (MMA M)
 constexpr int kN = 256;      // centroids (MMA N)
 constexpr int kNCls = 9;     // argmin classes = position inside a block of 7 or 9 centroids
 constexpr int kG = 8;        // max tiles per row group (codebook image reuse); the launch picks 1..kG
-constexpr int kGroups = 3;   // epilogue groups: item it belongs to group it % kGroups
+#ifndef CSPQ_TC_GROUPS
+#define CSPQ_TC_GROUPS 3
+#endif
+constexpr int kGroups = CSPQ_TC_GROUPS;   // epilogue groups: item it belongs to group it % kGroups
+constexpr int kLdCols = kGroups >= 4 ? 32 : 64;  // accumulator columns per tcgen05.ld (4 groups: 112 registers each)
 constexpr int kNA = 2 * kGroups;  // A-operand stages: a group alternates between two, so it writes the A rows of
                                   // its next item (it + kGroups) before it waits for item it's accumulator --
                                   // with one stage per group the next item's MMA could only start after the
@@ -90,8 +94,11 @@ constexpr int kNA = 2 * kGroups;  // A-operand stages: a group alternates betwee
 constexpr int kThreads = 128 + 128 * kGroups;  // warpgroup 0 = MMA warp, loader warp, two idle warps; then
                                                // kGroups epilogue warpgroups.  Warpgroup 0 hands its
                                                // registers to the epilogue (setmaxnreg kRegsLight / kRegsEpi)
-constexpr int kRegsLight = 40, kRegsEpi = 152;  // 128 x 40 + 384 x 152 = 63,488 <= 65,536
-static_assert(128 * kRegsLight + 128 * kGroups * kRegsEpi <= 65536, "register pool");
+// setmaxnreg moves registers inside the CTA's launch allocation (threads x the launch register count:
+// 512 x 128, or 640 x 96 with four groups), never beyond it
+constexpr int kRegsLight = 40, kRegsEpi = kGroups >= 4 ? 104 : 152;  // 128 x 40 + 384 x 152 = 63,488 <= 65,536
+constexpr int kRegsLaunch = (65536 / kThreads) / 8 * 8;
+static_assert(128 * kRegsLight + 128 * kGroups * kRegsEpi <= kThreads * kRegsLaunch, "register pool");
 // (Accumulator chunks -- N = 128 or 64 per MMA with per-chunk commits and barriers, so MMA and scan
 // overlap chunk by chunk -- were measured three times and never paid: c3 -4..-5 % with 2 chunks; an
 // N = 128 MMA costs what an N = 256 one does.)
@@ -148,6 +155,10 @@ __device__ __noinline__ long long mbar_wait_check(long long t0) {
     if (t - t0 > 20000000000ll) __trap();
     return t0;
 }
+#ifndef CSPQ_TC_WAIT_SLEEP
+#define CSPQ_TC_WAIT_SLEEP 0
+#endif
+template <int kSleepNs = 0>
 __device__ __forceinline__ void mbar_wait_s(uint32_t addr, uint32_t parity) {  // addr: shared address of the mbarrier
     // suspend (woken by the phase flip) instead of busy polling: spinning warps steal issue slots
     // from the epilogue warps that share their SM sub-partition.  A suspended try_wait also
@@ -163,6 +174,7 @@ __device__ __forceinline__ void mbar_wait_s(uint32_t addr, uint32_t parity) {  /
         asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
                      : "=r"(done) : "r"(addr), "r"(parity), "r"(kSuspendNs) : "memory");
         if (done) return;
+        if constexpr (kSleepNs > 0) asm volatile("nanosleep.u32 %0;" ::"n"(kSleepNs));
         if ((++spins & 255u) == 0) t0 = mbar_wait_check(t0);
     }
 }
@@ -211,7 +223,7 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
 }
 
 #define CSPQ_LD8(o) "=r"(v[o + 0]), "=r"(v[o + 1]), "=r"(v[o + 2]), "=r"(v[o + 3]), "=r"(v[o + 4]), "=r"(v[o + 5]), "=r"(v[o + 6]), "=r"(v[o + 7])
-__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t *v) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
         "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,"
@@ -219,6 +231,15 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
         "%57,%58,%59,%60,%61,%62,%63}, [%64];\n\t"
         "tcgen05.wait::ld.sync.aligned;"  // same statement: no use of v can be scheduled before the wait
         : CSPQ_LD8(0), CSPQ_LD8(8), CSPQ_LD8(16), CSPQ_LD8(24), CSPQ_LD8(32), CSPQ_LD8(40), CSPQ_LD8(48), CSPQ_LD8(56)
+        : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t *v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,"
+        "%29,%30,%31}, [%32];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : CSPQ_LD8(0), CSPQ_LD8(8), CSPQ_LD8(16), CSPQ_LD8(24)
         : "r"(taddr) : "memory");
 }
 #undef CSPQ_LD8
@@ -695,29 +716,32 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
 #pragma unroll
             for (int ch = 0; ch < 4 && !(probe & 1); ++ch) {
                 if (ch == 0) {
-                    mbar_wait_s(tf_s + 8 * (it & 3), (it >> 2) & 1);
+                    mbar_wait_s<CSPQ_TC_WAIT_SLEEP>(tf_s + 8 * (it & 3), (it >> 2) & 1);
                     if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 5] = clock64();
                     tc_fence_after();
                 }
-                uint32_t v[64];
-                tmem_ld64(tm_lane + tb * kN + ch * 64, v);
-                if (ch == 3) {  // the whole accumulator is in registers or reduced: hand the buffer back
+                float bmc[8];
+#pragma unroll
+                for (int half = 0; half < 64 / kLdCols; ++half) {
+                uint32_t v[kLdCols];
+                if constexpr (kLdCols == 64) tmem_ld64(tm_lane + tb * kN + ch * 64, v);
+                else tmem_ld32(tm_lane + tb * kN + ch * 64 + half * 32, v);
+                if (ch == 3 && half == 64 / kLdCols - 1) {  // the whole accumulator is in registers or reduced: hand the buffer back
                     tc_fence_before();
                     bar_arrive(kBarTEmpty + tb);
                     if (stamp && r == 0 && it < kStampItems) stamp[it * 8 + 4] = clock64();
                 }
 #define SV(i) __uint_as_float(v[(i)])
                 if (probe & 8) {
-                    cls[ch] = __fadd_rn(SV(0), SV(63));
+                    cls[ch] = __fadd_rn(SV(0), SV(kLdCols - 1));
                     continue;
                 }
                 // each 16 columns = a block of 7 then a block of 9 (3 + 4 three-input minima, no
                 // idle operand slot); the class is the position inside the block, so classes 0-6
                 // take two columns per 16 and classes 7-8 one (paired across 16-column groups)
-                float bmc[8];
 #pragma unroll
-                for (int bp = 0; bp < 4; ++bp) {
-                    const int o = 16 * bp;
+                for (int bq = 0; bq < kLdCols / 16; ++bq) {
+                    const int o = 16 * bq, bp = bq + half * (kLdCols / 16);
 #pragma unroll
                     for (int c = 0; c < 7; ++c) cls[c] = fmin3(cls[c], SV(o + c), SV(o + 7 + c));
                     if (bp & 1) {
@@ -728,12 +752,14 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
                     bmc[2 * bp + 1] = fmin3(fmin3(SV(o + 7), SV(o + 8), SV(o + 9)), fmin3(SV(o + 10), SV(o + 11), SV(o + 12)),
                                             fmin3(SV(o + 13), SV(o + 14), SV(o + 15)));
                 }
+#undef SV
+                }
+                if (probe & 8) continue;
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
                     sbm[2 * ch + h] = fmin3(fmin3(bmc[4 * h], bmc[4 * h + 1], bmc[4 * h + 2]), bmc[4 * h + 3], bmc[4 * h + 3]);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) scm[c] = fmin3(scm[c], bmc[c], bmc[4 + c]);
-#undef SV
             }
             if (probe & 1) {  // (timing probe: no TMEM reads; still walk the barriers)
                 mbar_wait_s(tf_s + 8 * (it & 3), (it >> 2) & 1);
