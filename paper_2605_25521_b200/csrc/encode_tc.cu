@@ -51,8 +51,10 @@
 //
 // Warp roles (128 + 128 kGroups threads, one CTA per SM, persistent over a contiguous range of
 // (row group, subspace) pairs).  The kernel is bound by issue slots: on this SM a half-rate
-// ALU-pipe instruction (FMNMX3: 276 of ~710 instructions per warp-item) holds a sub-partition's issue
-// port for two cycles (scripts/micro/issue_mix.cu), so time ~ 2 x ALU + other instructions.
+// ALU-pipe instruction (FMNMX3: 276 of ~600 instructions per warp-item; ~710 before the per-thread
+// addresses were made loop constants, see opaque32) holds a sub-partition's issue port for two cycles
+// (scripts/micro/issue_mix.cu), so time ~ 2 x ALU + other instructions.  More warps do not help:
+// four epilogue groups (-DCSPQ_TC_GROUPS=4) run 2-4 % slower.
 //   warps 0-3   one warpgroup that hands its registers to the others (setmaxnreg 40 / 152):
 //     warp 0    TMEM allocation + MMA issue (the warp walks the items, one elected lane issues);
 //               waits for A rows and drained accumulators on named barriers (bar.sync: no retries)
@@ -116,7 +118,7 @@ constexpr int kPD = 2;        // cp.async prefetch distance, in the group's own 
 constexpr int kRing = 3;      // x slots per group (> kPD: an item's slot outlives its fix-up)
 
 // error constant E of the tensor scores: |S - s_oracle| <= E W, W = max|b| + ||x|| max||c||
-// (tf32 split, 2 roundings per K = 8 step, the oracle's own chain; 1 % slack).  Lloyd's final
+// (fp16 hi/lo split, 2 roundings per 8 products, the oracle's own chain; 1 % slack).  Lloyd's final
 // REFERENCE screen widens the same band (lloyd.cu, final_guard_kernel)
 __host__ __device__ constexpr float tc_error_constant(int sub) {
     return (float)((4.0 / 4194304.0 + (sub == 8 ? 4 : 2) / 4194304.0 * (1.0 + 1.0 / 1024.0) + (sub + 1) / 16777216.0) * 1.01);
@@ -516,7 +518,7 @@ encode_tc_kernel(const TIn *__restrict__ X, int64_t n, int m, int64_t xs, int64_
             }
         }
     } else if (warp == 1) {
-        // ---------------- codebook loader: tf32 image (MMA) + fp32 codebook (fix-up) ----------------
+        // ---------------- codebook loader: fp16 image (MMA) + fp32 codebook (fix-up) ----------------
 #ifdef CSPQ_TC_STAMPS
         if (lane == 1 && stamp) {
             for (uint32_t it = 0; it < kStampItems; ++it) {

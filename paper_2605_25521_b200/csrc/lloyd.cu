@@ -88,7 +88,7 @@ struct WsLayout {
         tc_cb = take(4 * (int64_t)m * k * sub);
         tc_b = take(4 * (int64_t)m * k);
         tc_guard = take(8 * (int64_t)m);
-        tc_img = take((int64_t)m * k * 32 * 4);  // K = 32 tf32 per centroid row at most
+        tc_img = take((int64_t)m * k * 32 * 4);  // >= encode_tc_image_bytes (K = 32 fp16 per centroid row + the m scales)
         tc_codes = take((int64_t)m * n);
         tc_flags = take((int64_t)m * n);
         tc_rmax = take(4 * (int64_t)m);
