@@ -300,3 +300,16 @@ def test_fuzz_magnitudes_tensor(seed):
     r = subprocess.run([sys.executable, os.path.join(root, "scripts", "fuzz_tc_scales.py"), "80", str(seed)],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_fuzz_layouts_tensor(seed):
+    """scripts/fuzz_tc_layouts.py (random n / m / d_sub / input dtype, rows that are views into a wider
+    matrix, strided `out` rows): the tcgen05 kernel's codes equal the exact SIMT kernel's and nothing is
+    written beside them.  Guards the kernel's row-address arithmetic (per-thread bases + tile and
+    subspace multiples, `row < n` as a tile compare)."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "fuzz_tc_layouts.py"), "100", str(seed)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
