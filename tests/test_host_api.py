@@ -189,3 +189,25 @@ def test_tensor_kernel_subspace_limit_query():
         for dt in (N.IN_F32, N.IN_U8):
             assert L.cspq_encode_tc_max_subspaces(sub, dt) >= 256  # every configuration (m <= 192) fits
     assert L.cspq_encode_tc_max_subspaces(16, N.IN_F32) == 0
+
+
+def test_codebookset_from_rowmajor_batch_equals_per_subspace_construction():
+    """CodebookSet.from_rowmajor_batch builds the arrays of from_codebooks([Codebook.from_rowmajor ...])
+    bit for bit (the biases are part of the encode contract), and rejects what they reject."""
+    import numpy as np
+    import pytest
+    import paper_2605_25521_b200 as P
+    rng = np.random.default_rng(5)
+    for m, k, sub in [(1, 1, 1), (3, 7, 3), (16, 256, 8), (5, 256, 4), (2, 300, 16), (4, 33, 5)]:
+        C = (rng.standard_normal((m, k, sub)) * rng.choice([1e-3, 1.0, 300.0])).astype(np.float32)
+        a = P.CodebookSet.from_codebooks([P.Codebook.from_rowmajor(j, C[j]) for j in range(m)])
+        b = P.CodebookSet.from_rowmajor_batch(C)
+        for x, y in ((a.rowmajor, b.rowmajor), (a.transposed, b.transposed), (a.biases, b.biases)):
+            assert x.dtype == y.dtype and x.shape == y.shape and x.tobytes() == y.tobytes()
+            assert not y.flags.writeable
+    bad = np.zeros((3, 4, 2), np.float32)
+    bad[1, 2, 0] = np.nan
+    with pytest.raises(P.DataError, match="subspace 1"):
+        P.CodebookSet.from_rowmajor_batch(bad)
+    with pytest.raises(P.ConfigError):
+        P.CodebookSet.from_rowmajor_batch(np.zeros((4, 2), np.float32))
