@@ -83,7 +83,7 @@ namespace {
 constexpr int kTM = 128;     // rows per tile (MMA M)
 constexpr int kN = 256;      // centroids (MMA N)
 constexpr int kNCls = 9;     // argmin classes = position inside a block of 7 or 9 centroids
-constexpr int kG = 8;        // max tiles per row group (codebook image reuse); the launch picks 1..kG
+constexpr int kG = 16;       // max tiles per row group (codebook image reuse); the launch picks 1..kG
 #ifndef CSPQ_TC_GROUPS
 #define CSPQ_TC_GROUPS 3
 #endif
@@ -986,7 +986,9 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const flo
     const int64_t ntiles = (n + kTM - 1) / kTM;
     // tiles per row group: the CTAs share the (row group, subspace) pairs in contiguous ranges, so
     // the largest row group (kG tiles: the most codebook-image reuse) balances to within a pair
-    int gs = kG;
+    // 8 tiles; 16 for long uint8 / d_sub 4 launches (c4 +1.3 %; float32 rows: c3 -0.3 %, and 32 tiles
+    // c3 -27 %, c5 -48 %; short inputs lose balance: c1 -9 % at 16)
+    int gs = (sizeof(TIn) == 1 && SUB == 4 && ntiles >= (int64_t)sms * 64) ? 16 : 8;
     static const int gs_env = [] { const char *ge = getenv("CSPQ_TC_GS"); return ge ? atoi(ge) : 0; }();
     if (gs_env) gs = std::max(1, std::min(kG, gs_env));  // debug override
     const int64_t ngroups = (ntiles + gs - 1) / gs;
