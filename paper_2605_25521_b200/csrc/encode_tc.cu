@@ -986,9 +986,11 @@ int launch_tc(const TIn *X, int64_t n, int m, int64_t xs, int64_t xjs, const flo
     const int64_t ntiles = (n + kTM - 1) / kTM;
     // tiles per row group: the CTAs share the (row group, subspace) pairs in contiguous ranges, so
     // the largest row group (kG tiles: the most codebook-image reuse) balances to within a pair
-    // 8 tiles; 16 for long uint8 / d_sub 4 launches (c4 +1.3 %; float32 rows: c3 -0.3 %, and 32 tiles
-    // c3 -27 %, c5 -48 %; short inputs lose balance: c1 -9 % at 16)
-    int gs = (sizeof(TIn) == 1 && SUB == 4 && ntiles >= (int64_t)sms * 64) ? 16 : 8;
+    // 8 tiles.  16 for long uint8 / d_sub 4 launches ran 1.3 % faster on c4 but doubled its DRAM traffic
+    // (335 vs 168 B/row under ncu: a row's four sectors are fetched again by later subspaces once 16
+    // tiles x 148 CTAs of rows no longer stay in L2), so it is not the default; float32 rows: 16 tiles
+    // c3 -0.3 %, c1 -9 % (balance), 32 tiles c3 -27 %, c5 -48 %; 4 / 6 / 12 tiles within +-0.5 % of 8
+    int gs = 8;
     static const int gs_env = [] { const char *ge = getenv("CSPQ_TC_GS"); return ge ? atoi(ge) : 0; }();
     if (gs_env) gs = std::max(1, std::min(kG, gs_env));  // debug override
     const int64_t ngroups = (ntiles + gs - 1) / gs;

@@ -314,19 +314,3 @@ def test_fuzz_layouts_tensor(seed):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
-
-def test_long_uint8_launch_uses_wide_row_groups(P):
-    """uint8 / d_sub 4 launches of >= 64 tiles per SM take 16-tile row groups (encode_tc.cu, launch_tc):
-    the codes equal the exact SIMT kernel's, including the ragged last group and tile."""
-    import torch
-    dev = torch.device("cuda", 0)
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    n, m, sub = sms * 64 * 128 + 13 * 128 + 77, 32, 4
-    g = torch.Generator(device=dev).manual_seed(5)
-    X = torch.randint(0, 256, (n, m * sub), dtype=torch.uint8, device=dev, generator=g)
-    rows = X[torch.randint(0, n, (256,), device=dev, generator=g)].float().cpu().numpy()
-    rows += np.random.default_rng(5).standard_normal(rows.shape).astype(np.float32) * 3.0
-    cs = cset_of(P, rows.reshape(256, m, sub).transpose(1, 0, 2))
-    got = P.encode_dataset_device(X, cs, P.ExecutionPlan(mode="tensor"))
-    want = P.encode_dataset_device(X, cs, P.ExecutionPlan(mode="exact"))
-    assert torch.equal(got, want)
